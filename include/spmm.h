@@ -1,0 +1,192 @@
+/*
+ * spmm.h -- C ABI of libspmm.so: CSR sparse x tall-skinny row-major dense SpMM on B200 (sm_100a).
+ *
+ * The operation (§1, arXiv 1803.08601): "Given an m-by-k sparse matrix A and a k-by-n
+ * dense matrix B, SpMM computes an m-by-n dense matrix C = AB", A in CSR (§2.2: row
+ * offsets, column indices, values -- used as given, no format conversion), B and C
+ * dense row-major (Fig. 3 caption :107), n small (tall-skinny B).
+ * Generalised to the semirings plus-times and min-plus (GraphBLAS GrB_mxm framing).
+ *
+ * Two kernels and a selector:
+ *   SPMM_ALGO_ROWSPLIT  row splitting, §4.1 (Fig. 3, Table 1)
+ *   SPMM_ALGO_MERGE     merge-based, §4.2 Algorithm 1: PartitionSpmm (line 2),
+ *                       per-CTA compute with carry-out (lines 3-23), FixCarryOut (line 24)
+ *   SPMM_ALGO_AUTO      §5.4 heuristic: merge iff mean row length d = nnz/m < threshold
+ *                       (default 9.35), plus (policy AUTO) a skew guard, see spmm_plan_opts.
+ *
+ * Conventions (all entry points):
+ *   - Every pointer named row_offsets / col_indices / values / B / C / workspace is a DEVICE pointer
+ *     (cudaMalloc / torch CUDA memory) unless its name starts with host_.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Indices are int32 (m, k, nnz < 2^31); sizes are int64 for ABI stability.
+ *   - Errors are returned as spmm_status; no C++ exception crosses the ABI.  Kernel launch errors are
+ *     reported by the call that launched (SPMM_ERR_CUDA); asynchronous device faults surface at the
+ *     caller's next synchronisation of `stream`.
+ *   - Thread safety: a handle may be used from several host threads / streams concurrently only for
+ *     execute() with distinct workspaces; create/plan/destroy must not race with other calls on it.
+ */
+#ifndef SPMM_B200_H
+#define SPMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SPMM_API __attribute__((visibility("default")))
+#else
+#define SPMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMM_ABI_VERSION 1
+
+typedef struct spmm_csr_s* spmm_csr_t;
+
+typedef enum {
+    SPMM_OK = 0,
+    SPMM_ERR_NULL_POINTER = 1,        /* a required pointer argument is NULL                        */
+    SPMM_ERR_INVALID_ARG = 2,         /* bad size / leading dimension / enum / n != planned n        */
+    SPMM_ERR_INVALID_CSR = 3,         /* SPMM_FLAG_VALIDATE found a broken CSR invariant             */
+    SPMM_ERR_NOT_PLANNED = 4,         /* execute() before a successful plan()                        */
+    SPMM_ERR_WORKSPACE_TOO_SMALL = 5, /* workspace_bytes < the size plan() reported                 */
+    SPMM_ERR_UNSUPPORTED = 6,         /* n > 128, or a configuration this build does not implement  */
+    SPMM_ERR_CUDA = 7                 /* a CUDA runtime call or kernel launch failed                */
+} spmm_status;
+
+typedef enum { SPMM_ALGO_AUTO = 0, SPMM_ALGO_ROWSPLIT = 1, SPMM_ALGO_MERGE = 2 } spmm_algo;
+typedef enum { SPMM_F32 = 0, SPMM_I32 = 1 } spmm_dtype;                /* dtype of values, B and C */
+typedef enum { SPMM_PLUS_TIMES = 0, SPMM_MIN_PLUS = 1 } spmm_semiring;
+enum { SPMM_FLAG_VALIDATE = 1u };                                       /* one checking pass at create */
+
+typedef enum { SPMM_POLICY_AUTO = 0, SPMM_POLICY_PAPER = 1 } spmm_policy;
+typedef enum { SPMM_PARTITION_MERGE_PATH = 0, SPMM_PARTITION_NONZERO_SPLIT = 1 } spmm_partition;
+
+/* Optional planner knobs (spmm_csr_plan_ex).  Zero-initialised = defaults. */
+typedef struct {
+    int32_t policy;          /* spmm_policy.  PAPER: merge iff d < threshold.
+                                AUTO (default): PAPER rule, OR merge when the longest row exceeds
+                                the per-warp fair share nnz/(148*32) and is > 8x the mean
+                                (costs one O(m) device reduction + sync). */
+    int32_t partition;       /* spmm_partition for the merge kernel: 2-D merge path over (row ends,
+                                nonzeros) (default) or the paper's 1-D nonzero split
+                                (PAPER.md:80, :89).                                                  */
+    int32_t items_per_cta;   /* merge-path items (rows + nonzeros) per CTA; 0 = default (2048).
+                                Must be a multiple of 256 in [256, 16384].                           */
+    int32_t reserved[5];     /* must be zero */
+} spmm_plan_opts;
+
+/* Read-only description of the current plan (spmm_csr_get_plan_info). */
+typedef struct {
+    int64_t m, k, nnz;
+    int32_t n;
+    int32_t chosen;          /* spmm_algo actually used by execute (ROWSPLIT or MERGE) */
+    int32_t semiring, dtype, policy, partition;
+    double mean_row_length;  /* d = nnz/m */
+    int64_t max_row_length;  /* -1 unless computed (AUTO policy) */
+    double threshold;
+    int32_t num_ctas;        /* CTAs of the compute kernel */
+    int32_t items_per_cta;   /* merge only */
+    int32_t launches_per_execute;  /* kernels one execute() enqueues (row split 1, merge 3) */
+    int32_t reserved0;
+    size_t workspace_bytes;
+} spmm_plan_info;
+
+/*
+ * spmm_csr_create -- record a CSR matrix A (m x k, nnz stored entries).  a0 in SURVEY.md §8(a).
+ *   row_offsets[m+1], col_indices[nnz], values[nnz]: device arrays, BORROWED (never copied or
+ *   converted); they must stay valid and unmodified until spmm_csr_destroy.
+ *   values has the element type `dtype` (float or int32).  Column indices need not be sorted or
+ *   unique within a row (duplicates are summed in storage order).
+ *   flags: SPMM_FLAG_VALIDATE runs one synchronous device pass checking row_offsets[0] == 0,
+ *   non-decreasing offsets, row_offsets[m] == nnz and 0 <= col < k (else SPMM_ERR_INVALID_CSR).
+ *   Without it the CSR is trusted.  m == 0 or nnz == 0 is allowed (pointers may then be NULL
+ *   except row_offsets when m > 0).  k == 0 requires nnz == 0.
+ *   *out receives a new handle (owned by the caller, free with spmm_csr_destroy).
+ */
+SPMM_API spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz,
+                            const int32_t* row_offsets, const int32_t* col_indices, const void* values,
+                            spmm_dtype dtype, uint32_t flags, void* stream);
+
+/*
+ * spmm_csr_plan -- choose the kernel for B with n columns (1 <= n <= 128) and size the workspace.
+ *   algo_or_auto: force ROWSPLIT / MERGE, or AUTO (§5.4 heuristic).
+ *   threshold <= 0 -> 9.35.  *workspace_bytes receives the device workspace size
+ *   execute() needs (0 for row split); *chosen receives ROWSPLIT or MERGE.  Either out pointer may
+ *   be NULL.  Plan with AUTO policy enqueues one reduction on `stream` and synchronises it.
+ */
+SPMM_API spmm_status spmm_csr_plan(spmm_csr_t h, int32_t n, spmm_algo algo_or_auto, spmm_semiring sr,
+                          double threshold, void* stream, size_t* workspace_bytes, spmm_algo* chosen);
+
+/* spmm_csr_plan with explicit planner options (opts may be NULL = defaults). */
+SPMM_API spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo_or_auto, spmm_semiring sr,
+                             double threshold, const spmm_plan_opts* opts, void* stream,
+                             size_t* workspace_bytes, spmm_algo* chosen);
+
+/*
+ * spmm_csr_execute -- C = A (x) B over the planned semiring, enqueued on `stream`, no host sync,
+ * no allocation.
+ *   B: device, k rows x ldb (row-major, element = dtype); only columns [0, n) are read, and only
+ *      rows named by col_indices.  C: device, m rows x ldc; columns [0, n) of every row are
+ *      OVERWRITTEN (no alpha/beta: the paper computes C = AB); columns [n, ldc) are
+ *      untouched.  Empty rows receive the semiring identity (0, +inf or INT32_MAX).
+ *   Requires ldb >= n, ldc >= n, n == planned n.  B and C must not overlap.  16-byte aligned B/C
+ *   with ldb/ldc multiples of 4 take the float4 path; anything else takes a narrower vector or
+ *   scalar path with bit-identical results for int32 / min-plus.
+ *   workspace: device buffer of at least the planned workspace_bytes (may be NULL if 0), 16-byte
+ *   aligned, caller-owned, not shared by concurrent executes.
+ */
+SPMM_API spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* spmm_csr_destroy -- free the handle (not the borrowed CSR arrays).  NULL is a no-op. */
+SPMM_API spmm_status spmm_csr_destroy(spmm_csr_t h);
+
+/* Fill *out with the current plan (SPMM_ERR_NOT_PLANNED before plan). */
+SPMM_API spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out);
+
+/*
+ * spmm_csr_set_timing_events -- diagnostic: if count > 0, every later execute() records
+ * events[0] (cudaEvent_t) on its stream before its first kernel and events[i+1] after its i-th
+ * kernel (i < count-1), so the caller can time each kernel of the path separately (the bench's
+ * roofline uses the dominant kernel's own duration).  count == 0 disables.  The events are borrowed.
+ */
+SPMM_API spmm_status spmm_csr_set_timing_events(spmm_csr_t h, void* const* events, int32_t count);
+
+/* Static strings; never NULL. */
+SPMM_API const char* spmm_status_string(spmm_status s);
+SPMM_API const char* spmm_csr_last_error(spmm_csr_t h);   /* per-handle detail message of the last failure */
+SPMM_API int32_t spmm_abi_version(void);
+
+/*
+ * spmm_merge_partition -- the merge kernel's phase 1 (Alg. 1 line 2 "PartitionSpmm")
+ * on its own, exported for verification.  For each c in [0, num_ctas] writes the merge-path state
+ * (row, nonzero) at which CTA c starts (c == num_ctas: the end state (m, nnz)):
+ *   partition == MERGE_PATH: state on diagonal min(c*items_per_cta, m+nnz) of the merge of row-end
+ *       offsets with nonzero indices, rows first on ties (Fig. 2(c));
+ *   partition == NONZERO_SPLIT: (largest r with row_offsets[r] <= c*items_per_cta, c*items_per_cta),
+ *       row 0 for c == 0 (SURVEY.md §8(c) ambiguity 20b).
+ * num_ctas must equal spmm_merge_num_ctas(m, nnz, items_per_cta, partition).
+ * row_offsets: device int32[m+1]; states_out: device int32[2*(num_ctas+1)] as (row, nz) pairs.
+ */
+SPMM_API int64_t spmm_merge_num_ctas(int64_t m, int64_t nnz, int32_t items_per_cta, int32_t partition);
+SPMM_API spmm_status spmm_merge_partition(const int32_t* row_offsets, int64_t m, int64_t nnz, int32_t items_per_cta,
+                                 int32_t partition, int64_t num_ctas, int32_t* states_out, void* stream);
+
+/*
+ * spmm_partition_rows -- host-side 1-D row-block partition for multi-GPU SpMM (north_star;
+ * SURVEY.md §8(e)).  host_row_offsets: HOST int32[m+1].  Writes parts+1 row bounds (int64, host):
+ * bounds[0] = 0, bounds[parts] = m, non-decreasing; part p owns rows [bounds[p], bounds[p+1]).
+ *   mode 0: nnz-balanced, bounds[p] = first row r with row_offsets[r] >= p*nnz/parts (lower_bound);
+ *   mode 1: merge-path balanced, bounds[p] = row coordinate of diagonal p*(m+nnz)/parts.
+ * A row is never split across parts.
+ */
+SPMM_API spmm_status spmm_partition_rows(const int32_t* host_row_offsets, int64_t m, int32_t parts, int32_t mode,
+                                int64_t* row_bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMM_B200_H */

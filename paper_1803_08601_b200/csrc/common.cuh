@@ -1,0 +1,132 @@
+// common.cuh -- semiring arithmetic, vector gathers and cache-hinted memory ops shared by the
+// sm_100a SpMM kernels (row split, merge path, carry fix-up).  Product code; shares nothing with
+// oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spmm {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WARPS_PER_CTA = 8;          // 256-thread CTAs everywhere
+constexpr int THREADS = 32 * WARPS_PER_CTA;
+
+enum : int { SR_PLUS_TIMES = 0, SR_MIN_PLUS = 1 };
+
+// ---------------------------------------------------------------------------------------------
+// Semirings (GrB_mxm framing).  mac(acc, a, b) = acc (+) (a (x) b); add = (+).
+// int32 arithmetic is done in uint32 so overflow wraps (SURVEY.md §8(c) ambiguity 19).
+// ---------------------------------------------------------------------------------------------
+template <typename T, int SR> struct Ring;
+
+template <> struct Ring<float, SR_PLUS_TIMES> {
+    __device__ __forceinline__ static float id() { return 0.0f; }
+    __device__ __forceinline__ static float mac(float acc, float a, float b) { return __fmaf_rn(a, b, acc); }
+    __device__ __forceinline__ static float add(float x, float y) { return __fadd_rn(x, y); }
+};
+template <> struct Ring<int, SR_PLUS_TIMES> {
+    __device__ __forceinline__ static int id() { return 0; }
+    __device__ __forceinline__ static int mac(int acc, int a, int b) {
+        return (int)((unsigned)acc + (unsigned)a * (unsigned)b);
+    }
+    __device__ __forceinline__ static int add(int x, int y) { return (int)((unsigned)x + (unsigned)y); }
+};
+template <> struct Ring<float, SR_MIN_PLUS> {
+    __device__ __forceinline__ static float id() { return __int_as_float(0x7f800000); }
+    __device__ __forceinline__ static float mac(float acc, float a, float b) { return fminf(acc, __fadd_rn(a, b)); }
+    __device__ __forceinline__ static float add(float x, float y) { return fminf(x, y); }
+};
+template <> struct Ring<int, SR_MIN_PLUS> {
+    __device__ __forceinline__ static int id() { return 0x7fffffff; }
+    __device__ __forceinline__ static int mac(int acc, int a, int b) {
+        return min(acc, (int)((unsigned)a + (unsigned)b));
+    }
+    __device__ __forceinline__ static int add(int x, int y) { return min(x, y); }
+};
+
+// ---------------------------------------------------------------------------------------------
+// bit casts
+// ---------------------------------------------------------------------------------------------
+template <typename T> __device__ __forceinline__ T from_bits(unsigned u);
+template <> __device__ __forceinline__ float from_bits<float>(unsigned u) { return __uint_as_float(u); }
+template <> __device__ __forceinline__ int from_bits<int>(unsigned u) { return (int)u; }
+template <typename T> __device__ __forceinline__ unsigned to_bits(T v);
+template <> __device__ __forceinline__ unsigned to_bits<float>(float v) { return __float_as_uint(v); }
+template <> __device__ __forceinline__ unsigned to_bits<int>(int v) { return (unsigned)v; }
+
+// ---------------------------------------------------------------------------------------------
+// Memory ops.
+//   A stream (col_indices, values, row_offsets): read once -> no L1 allocation.
+//   B gathers: read-only path (L1 + L2 cached); B rows are the reused operand.
+//   C rows: written once -> streaming store (evict-first).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ int ld_stream(const int* p) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ unsigned ld_stream_u(const void* p) {
+    unsigned v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// gather VEC consecutive elements of a B row (VEC in {1,2,4}); p must be VEC*4-byte aligned
+template <int VEC> __device__ __forceinline__ void ldg_vec(unsigned (&o)[VEC], const void* p);
+template <> __device__ __forceinline__ void ldg_vec<1>(unsigned (&o)[1], const void* p) {
+    o[0] = __ldg(reinterpret_cast<const unsigned*>(p));
+}
+template <> __device__ __forceinline__ void ldg_vec<2>(unsigned (&o)[2], const void* p) {
+    uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    o[0] = v.x; o[1] = v.y;
+}
+template <> __device__ __forceinline__ void ldg_vec<4>(unsigned (&o)[4], const void* p) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+
+template <int VEC> __device__ __forceinline__ void st_vec(void* p, const unsigned (&o)[VEC]);
+template <> __device__ __forceinline__ void st_vec<1>(void* p, const unsigned (&o)[1]) {
+    __stcs(reinterpret_cast<unsigned*>(p), o[0]);
+}
+template <> __device__ __forceinline__ void st_vec<2>(void* p, const unsigned (&o)[2]) {
+    __stcs(reinterpret_cast<uint2*>(p), make_uint2(o[0], o[1]));
+}
+template <> __device__ __forceinline__ void st_vec<4>(void* p, const unsigned (&o)[4]) {
+    __stcs(reinterpret_cast<uint4*>(p), make_uint4(o[0], o[1], o[2], o[3]));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Warp-cooperative 32-ary search: first x in [lo, hi) with pred(x) true (pred monotone
+// false..true), or hi if none.  ~log32(hi-lo) rounds of one coalesced-ish probe per lane.
+// All 32 lanes must call it with identical arguments.
+// ---------------------------------------------------------------------------------------------
+template <class Pred>
+__device__ __forceinline__ long long warp_search_first(long long lo, long long hi, Pred pred) {
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 32) {
+        const long long step = (hi - lo + 31) / 32;
+        const long long x = lo + lane * step;
+        const bool p = (x >= hi) || pred(x);
+        const unsigned b = __ballot_sync(FULL, p);
+        if (b == 0u) {
+            lo = lo + 31 * step + 1;
+        } else {
+            const int f = __ffs(b) - 1;
+            if (f == 0) {
+                hi = lo;
+            } else {
+                const long long xf = lo + f * step;
+                lo = lo + (long long)(f - 1) * step + 1;
+                hi = xf < hi ? xf : hi;
+            }
+        }
+    }
+    const long long x = lo + lane;
+    const bool p = (x >= hi) || pred(x);
+    const unsigned b = __ballot_sync(FULL, p);
+    return b ? lo + (__ffs(b) - 1) : hi;
+}
+
+}  // namespace spmm

@@ -1,0 +1,483 @@
+// spmm_api.cu -- the C ABI of libspmm.so (include/spmm.h): handle, planner, §5.4 heuristic,
+// workspace sizing, argument checks and kernel dispatch for the sm_100a CSR SpMM kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/spmm.h"
+#include "common.cuh"
+#include "merge.cuh"
+#include "rowsplit.cuh"
+
+using namespace spmm;
+
+struct spmm_csr_s {
+    int64_t m = 0, k = 0, nnz = 0;
+    const int32_t* ro = nullptr;
+    const int32_t* col = nullptr;
+    const void* val = nullptr;
+    spmm_dtype dtype = SPMM_F32;
+    // plan
+    bool planned = false;
+    int32_t n = 0;
+    spmm_algo chosen = SPMM_ALGO_ROWSPLIT;
+    spmm_semiring sr = SPMM_PLUS_TIMES;
+    spmm_plan_opts opts{};
+    double threshold = 9.35;
+    int64_t max_row = -1;
+    int64_t num_ctas = 0;
+    int32_t items = 2048;
+    int32_t rounds = 4;
+    size_t ws_bytes = 0;
+    int* d_scratch = nullptr;  // 16 bytes: plan-time reduction / validation flags
+    cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
+    int32_t nev = 0;
+    std::string err;
+};
+
+namespace {
+
+constexpr int kDefaultItems = 2048;
+constexpr int kNumSMs = 148;
+constexpr int kRowsplitU = 8;
+constexpr int kMergeU = 8;
+
+spmm_status fail(spmm_csr_t h, spmm_status s, const std::string& msg) {
+    if (h) h->err = msg;
+    return s;
+}
+
+spmm_status cuda_fail(spmm_csr_t h, cudaError_t e, const char* where) {
+    if (h) h->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return SPMM_ERR_CUDA;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline void mark(const spmm_csr_s* h, int i, cudaStream_t st) {
+    if (i < h->nev && h->ev[i]) cudaEventRecord(h->ev[i], st);
+}
+
+// ------------------------------------------------------------------------------------------------
+// device helpers for create/plan
+// ------------------------------------------------------------------------------------------------
+__global__ void k_max_row(const int* __restrict__ ro, long long m, int* __restrict__ out) {
+    int best = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+        best = max(best, ro[i + 1] - ro[i]);
+    best = __reduce_max_sync(FULL, best);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// flags: bit0 ro[0] != 0, bit1 decreasing offsets, bit2 ro[m] != nnz, bit3 column out of range
+__global__ void k_validate(const int* __restrict__ ro, long long m, long long nnz, const int* __restrict__ col,
+                           long long k, int* __restrict__ flags) {
+    int f = 0;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long step = (long long)gridDim.x * blockDim.x;
+    if (tid == 0) {
+        if (ro[0] != 0) f |= 1;
+        if ((long long)ro[m] != nnz) f |= 4;
+    }
+    for (long long i = tid; i < m; i += step)
+        if (ro[i + 1] < ro[i]) f |= 2;
+    for (long long p = tid; p < nnz; p += step) {
+        const int c = col[p];
+        if (c < 0 || (long long)c >= k) f |= 8;
+    }
+    if (f) atomicOr(flags, f);
+}
+
+int pow2ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+struct VecCfg {
+    int vec, G, NV;
+};
+
+VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, bool folded) {
+    const uintptr_t pb = (uintptr_t)B, pc = (uintptr_t)C;
+    int vec = 1;
+    if (n % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && pb % 16 == 0 && pc % 16 == 0) vec = 4;
+    else if (n % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0 && pb % 8 == 0 && pc % 8 == 0) vec = 2;
+    const int lanes = (n + vec - 1) / vec;
+    VecCfg c;
+    c.vec = vec;
+    if (folded) {
+        c.G = std::min(32, pow2ceil(lanes));
+        c.NV = (lanes + 31) / 32;
+    } else {
+        c.G = 32;
+        c.NV = (lanes + 31) / 32;
+    }
+    return c;
+}
+
+// ------------------------------------------------------------------------------------------------
+// dispatch tables
+// ------------------------------------------------------------------------------------------------
+template <typename T, int SR>
+cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, const T* B, long long ldb, T* C, long long ldc,
+                            cudaStream_t st) {
+    const int S = 32 / cfg.G;
+    const long long rows_per_cta = (long long)WARPS_PER_CTA * S * h->rounds;
+    const long long grid = (h->m + rows_per_cta - 1) / rows_per_cta;
+    if (grid <= 0) return cudaSuccess;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    const int m = (int)h->m, n = h->n;
+    const T* val = static_cast<const T*>(h->val);
+#define RS_CASE(V, G_, NV_)                                                                                   \
+    case (V)*1000 + (G_)*10 + (NV_):                                                                          \
+        k_rowsplit<T, SR, V, G_, NV_, kRowsplitU><<<(unsigned)grid, THREADS, 0, st>>>(m, n, h->ro, h->col, val, \
+                                                                                     B, ldb, C, ldc, h->rounds); \
+        break;
+    mark(h, 0, st);
+    switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
+        RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 16, 1) RS_CASE(4, 32, 1)
+        RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 16, 1) RS_CASE(2, 32, 1)
+        RS_CASE(2, 32, 2)
+        RS_CASE(1, 1, 1) RS_CASE(1, 2, 1) RS_CASE(1, 4, 1) RS_CASE(1, 8, 1) RS_CASE(1, 16, 1) RS_CASE(1, 32, 1)
+        RS_CASE(1, 32, 2) RS_CASE(1, 32, 3) RS_CASE(1, 32, 4)
+        default: return cudaErrorNotSupported;
+    }
+#undef RS_CASE
+    mark(h, 1, st);
+    return cudaGetLastError();
+}
+
+template <typename T, int SR>
+cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, const T* B, long long ldb, T* C, long long ldc,
+                         unsigned char* ws, cudaStream_t st) {
+    const long long NC = h->num_ctas;
+    if (NC <= 0) return cudaSuccess;
+    int* states = reinterpret_cast<int*>(ws);
+    size_t off = align256(sizeof(int) * 2 * (NC + 1));
+    int* carry_row = reinterpret_cast<int*>(ws + off);
+    off += align256(sizeof(int) * NC);
+    int* carry_flag = reinterpret_cast<int*>(ws + off);
+    off += align256(sizeof(int) * NC);
+    T* carry_val = reinterpret_cast<T*>(ws + off);
+    const int m = (int)h->m, n = h->n, nnz = (int)h->nnz, items = h->items;
+    // phase 1: PartitionSpmm (Alg. 1 line 2)
+    const long long pgrid = (NC + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+    mark(h, 0, st);
+    k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, m, nnz, items, h->opts.partition, (int)NC, states);
+    mark(h, 1, st);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // phase 2: per-CTA compute + carry-out (Alg. 1 lines 3-23)
+    const size_t smem = merge_smem_bytes(items, n, (int)sizeof(T));
+    const T* val = static_cast<const T*>(h->val);
+#define MG_CASE(V, NV_)                                                                                  \
+    case (V)*10 + (NV_): {                                                                               \
+        auto kfn = k_merge<T, SR, V, NV_, kMergeU>;                                                       \
+        if (smem > 48 * 1024) {                                                                          \
+            e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+            if (e != cudaSuccess) return e;                                                              \
+        }                                                                                                \
+        kfn<<<(unsigned)NC, THREADS, smem, st>>>(m, n, nnz, h->ro, h->col, val, B, ldb, C, ldc, states, items, \
+                                                 carry_row, carry_flag, carry_val);                      \
+        break;                                                                                           \
+    }
+    switch (cfg.vec * 10 + cfg.NV) {
+        MG_CASE(4, 1) MG_CASE(2, 1) MG_CASE(2, 2) MG_CASE(1, 1) MG_CASE(1, 2) MG_CASE(1, 3) MG_CASE(1, 4)
+        default: return cudaErrorNotSupported;
+    }
+#undef MG_CASE
+    mark(h, 2, st);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // phase 3: FixCarryOut (Alg. 1 line 24)
+    const long long fgrid = (NC + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+    k_fixup<T, SR><<<(unsigned)fgrid, THREADS, 0, st>>>((int)NC, n, carry_row, carry_flag, carry_val, C, ldc);
+    mark(h, 3, st);
+    return cudaGetLastError();
+}
+
+template <typename T, int SR>
+cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, long long ldc, void* ws,
+                cudaStream_t st) {
+    const T* B = static_cast<const T*>(Bv);
+    T* C = static_cast<T*>(Cv);
+    if (h->chosen == SPMM_ALGO_ROWSPLIT)
+        return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), B, ldb, C, ldc, st);
+    return launch_merge<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, false), B, ldb, C, ldc,
+                               static_cast<unsigned char*>(ws), st);
+}
+
+}  // namespace
+
+// ================================================================================================
+// C ABI
+// ================================================================================================
+extern "C" {
+
+int32_t spmm_abi_version(void) { return SPMM_ABI_VERSION; }
+
+const char* spmm_status_string(spmm_status s) {
+    switch (s) {
+        case SPMM_OK: return "SPMM_OK";
+        case SPMM_ERR_NULL_POINTER: return "SPMM_ERR_NULL_POINTER: a required pointer argument is NULL";
+        case SPMM_ERR_INVALID_ARG: return "SPMM_ERR_INVALID_ARG: invalid size, leading dimension or enum";
+        case SPMM_ERR_INVALID_CSR: return "SPMM_ERR_INVALID_CSR: CSR invariant violated";
+        case SPMM_ERR_NOT_PLANNED: return "SPMM_ERR_NOT_PLANNED: execute before plan";
+        case SPMM_ERR_WORKSPACE_TOO_SMALL: return "SPMM_ERR_WORKSPACE_TOO_SMALL";
+        case SPMM_ERR_UNSUPPORTED: return "SPMM_ERR_UNSUPPORTED: configuration not implemented (n > 128?)";
+        case SPMM_ERR_CUDA: return "SPMM_ERR_CUDA: CUDA runtime error";
+    }
+    return "unknown spmm_status";
+}
+
+const char* spmm_csr_last_error(spmm_csr_t h) {
+    if (!h) return "null handle";
+    return h->err.c_str();
+}
+
+spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, const int32_t* row_offsets,
+                            const int32_t* col_indices, const void* values, spmm_dtype dtype, uint32_t flags,
+                            void* stream) {
+    if (!out) return SPMM_ERR_NULL_POINTER;
+    *out = nullptr;
+    if (m < 0 || k < 0 || nnz < 0 || m >= 0x7fffffffLL || k >= 0x7fffffffLL || nnz >= 0x7fffffffLL ||
+        m + nnz >= 0x7fffffffLL)
+        return SPMM_ERR_INVALID_ARG;
+    if (k == 0 && nnz != 0) return SPMM_ERR_INVALID_ARG;
+    if (dtype != SPMM_F32 && dtype != SPMM_I32) return SPMM_ERR_INVALID_ARG;
+    if ((flags & ~SPMM_FLAG_VALIDATE) != 0u) return SPMM_ERR_INVALID_ARG;
+    if (m > 0 && !row_offsets) return SPMM_ERR_NULL_POINTER;
+    if (nnz > 0 && (!col_indices || !values)) return SPMM_ERR_NULL_POINTER;
+    spmm_csr_s* h = new (std::nothrow) spmm_csr_s();
+    if (!h) return SPMM_ERR_CUDA;
+    h->m = m; h->k = k; h->nnz = nnz;
+    h->ro = row_offsets; h->col = col_indices; h->val = values; h->dtype = dtype;
+    cudaError_t e = cudaMalloc(&h->d_scratch, 16);
+    if (e != cudaSuccess) { delete h; return SPMM_ERR_CUDA; }
+    if ((flags & SPMM_FLAG_VALIDATE) && m > 0) {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int hflags = 0;
+        e = cudaMemsetAsync(h->d_scratch, 0, 16, st);
+        if (e == cudaSuccess) {
+            const long long work = std::max<long long>(m, nnz);
+            const int grid = (int)std::min<long long>((work + THREADS - 1) / THREADS, 8LL * kNumSMs);
+            k_validate<<<std::max(grid, 1), THREADS, 0, st>>>(row_offsets, m, nnz, col_indices, k, h->d_scratch);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&hflags, h->d_scratch, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            cudaFree(h->d_scratch);
+            delete h;
+            return SPMM_ERR_CUDA;
+        }
+        if (hflags) {
+            cudaFree(h->d_scratch);
+            delete h;
+            return SPMM_ERR_INVALID_CSR;
+        }
+    }
+    *out = h;
+    return SPMM_OK;
+}
+
+spmm_status spmm_csr_destroy(spmm_csr_t h) {
+    if (!h) return SPMM_OK;
+    if (h->d_scratch) cudaFree(h->d_scratch);
+    delete h;
+    return SPMM_OK;
+}
+
+int64_t spmm_merge_num_ctas(int64_t m, int64_t nnz, int32_t items_per_cta, int32_t partition) {
+    if (items_per_cta <= 0 || m < 0 || nnz < 0) return -1;
+    if (m + nnz == 0) return 0;
+    if (partition == SPMM_PARTITION_NONZERO_SPLIT) return std::max<int64_t>(1, (nnz + items_per_cta - 1) / items_per_cta);
+    return (m + nnz + items_per_cta - 1) / items_per_cta;
+}
+
+spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semiring sr, double threshold,
+                             const spmm_plan_opts* opts, void* stream, size_t* workspace_bytes, spmm_algo* chosen) {
+    if (!h) return SPMM_ERR_NULL_POINTER;
+    h->planned = false;
+    if (n < 1) return fail(h, SPMM_ERR_INVALID_ARG, "n must be >= 1");
+    if (n > 128) return fail(h, SPMM_ERR_UNSUPPORTED, "n > 128 is not implemented (SURVEY.md §8(b))");
+    if (algo != SPMM_ALGO_AUTO && algo != SPMM_ALGO_ROWSPLIT && algo != SPMM_ALGO_MERGE)
+        return fail(h, SPMM_ERR_INVALID_ARG, "bad algo");
+    if (sr != SPMM_PLUS_TIMES && sr != SPMM_MIN_PLUS) return fail(h, SPMM_ERR_INVALID_ARG, "bad semiring");
+    spmm_plan_opts o{};
+    if (opts) o = *opts;
+    for (int i = 0; i < 5; ++i)
+        if (o.reserved[i] != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
+    if (o.policy != SPMM_POLICY_AUTO && o.policy != SPMM_POLICY_PAPER) return fail(h, SPMM_ERR_INVALID_ARG, "bad policy");
+    if (o.partition != SPMM_PARTITION_MERGE_PATH && o.partition != SPMM_PARTITION_NONZERO_SPLIT)
+        return fail(h, SPMM_ERR_INVALID_ARG, "bad partition");
+    int items = o.items_per_cta ? o.items_per_cta : kDefaultItems;
+    if (items < 256 || items > 16384 || items % 256 != 0)
+        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 256 in [256, 16384]");
+    o.items_per_cta = items;
+    h->threshold = threshold > 0 ? threshold : 9.35;
+    h->n = n;
+    h->sr = sr;
+    h->opts = o;
+    h->items = items;
+    h->max_row = -1;
+    const double d = h->m > 0 ? (double)h->nnz / (double)h->m : 0.0;  // PAPER.md:267, mean row length
+    spmm_algo pick = algo;
+    if (algo == SPMM_ALGO_AUTO) {
+        // §5.4: "use merge-based on datasets whose mean row length is less than 9.35, and row split otherwise"
+        pick = (d < h->threshold) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
+        if (pick == SPMM_ALGO_ROWSPLIT && o.policy == SPMM_POLICY_AUTO && h->m > 0) {
+            // skew guard: a row longer than the per-warp fair share makes row split a
+            // straggler (Type 1 imbalance); merge path balances it.
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            int hmax = 0;
+            cudaError_t e = cudaMemsetAsync(h->d_scratch, 0, sizeof(int), st);
+            if (e == cudaSuccess) {
+                const int grid = (int)std::min<long long>((h->m + THREADS - 1) / THREADS, 8LL * kNumSMs);
+                k_max_row<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->m, h->d_scratch);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&hmax, h->d_scratch, sizeof(int), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_fail(h, e, "plan: max row length");
+            h->max_row = hmax;
+            const double fair = (double)h->nnz / (double)(kNumSMs * 32);
+            if ((double)hmax > fair && (double)hmax > 8.0 * d) pick = SPMM_ALGO_MERGE;
+        }
+    }
+    h->chosen = pick;
+    h->ws_bytes = 0;
+    h->num_ctas = 0;
+    if (pick == SPMM_ALGO_MERGE) {
+        const int64_t NC = spmm_merge_num_ctas(h->m, h->nnz, items, o.partition);
+        h->num_ctas = NC;
+        if (NC > 0) {
+            const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
+            h->ws_bytes = align256(sizeof(int) * 2 * (NC + 1)) + 2 * align256(sizeof(int) * NC) +
+                          align256(elem * (size_t)NC * n);
+        }
+    } else {
+        const int S = 32 / std::min(32, pow2ceil((n + 3) / 4));
+        const long long rpc = (long long)WARPS_PER_CTA * S * h->rounds;
+        h->num_ctas = (h->m + rpc - 1) / rpc;
+    }
+    h->planned = true;
+    if (workspace_bytes) *workspace_bytes = h->ws_bytes;
+    if (chosen) *chosen = pick;
+    return SPMM_OK;
+}
+
+spmm_status spmm_csr_plan(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semiring sr, double threshold, void* stream,
+                          size_t* workspace_bytes, spmm_algo* chosen) {
+    return spmm_csr_plan_ex(h, n, algo, sr, threshold, nullptr, stream, workspace_bytes, chosen);
+}
+
+spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
+    if (!h || !out) return SPMM_ERR_NULL_POINTER;
+    if (!h->planned) return fail(h, SPMM_ERR_NOT_PLANNED, "not planned");
+    std::memset(out, 0, sizeof(*out));
+    out->m = h->m; out->k = h->k; out->nnz = h->nnz; out->n = h->n;
+    out->chosen = h->chosen; out->semiring = h->sr; out->dtype = h->dtype;
+    out->policy = h->opts.policy; out->partition = h->opts.partition;
+    out->mean_row_length = h->m > 0 ? (double)h->nnz / (double)h->m : 0.0;
+    out->max_row_length = h->max_row;
+    out->threshold = h->threshold;
+    out->num_ctas = (int32_t)h->num_ctas;
+    out->items_per_cta = h->chosen == SPMM_ALGO_MERGE ? h->items : 0;
+    out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : 1);
+    out->workspace_bytes = h->ws_bytes;
+    return SPMM_OK;
+}
+
+spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+    if (!h) return SPMM_ERR_NULL_POINTER;
+    if (!h->planned) return fail(h, SPMM_ERR_NOT_PLANNED, "execute before plan");
+    if (n != h->n) return fail(h, SPMM_ERR_INVALID_ARG, "n differs from the planned n");
+    if (ldb < n || ldc < n) return fail(h, SPMM_ERR_INVALID_ARG, "ldb and ldc must be >= n");
+    if (h->m == 0) return SPMM_OK;
+    if (!C) return fail(h, SPMM_ERR_NULL_POINTER, "C is NULL");
+    if (h->nnz > 0 && !B) return fail(h, SPMM_ERR_NULL_POINTER, "B is NULL");
+    if (workspace_bytes < h->ws_bytes) return fail(h, SPMM_ERR_WORKSPACE_TOO_SMALL, "workspace too small");
+    if (h->ws_bytes > 0 && !workspace) return fail(h, SPMM_ERR_NULL_POINTER, "workspace is NULL");
+    if (h->ws_bytes > 0 && ((uintptr_t)workspace % 16) != 0)
+        return fail(h, SPMM_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
+    if ((long long)h->m * ldc >= (1LL << 40) || (long long)h->k * ldb >= (1LL << 40))
+        return fail(h, SPMM_ERR_UNSUPPORTED, "matrix too large");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (h->dtype == SPMM_F32) {
+        e = (h->sr == SPMM_PLUS_TIMES) ? run<float, SR_PLUS_TIMES>(h, B, ldb, C, ldc, workspace, st)
+                                       : run<float, SR_MIN_PLUS>(h, B, ldb, C, ldc, workspace, st);
+    } else {
+        e = (h->sr == SPMM_PLUS_TIMES) ? run<int, SR_PLUS_TIMES>(h, B, ldb, C, ldc, workspace, st)
+                                       : run<int, SR_MIN_PLUS>(h, B, ldb, C, ldc, workspace, st);
+    }
+    if (e == cudaErrorNotSupported) return fail(h, SPMM_ERR_UNSUPPORTED, "no kernel instance for this n / alignment");
+    if (e != cudaSuccess) return cuda_fail(h, e, "execute");
+    return SPMM_OK;
+}
+
+spmm_status spmm_csr_set_timing_events(spmm_csr_t h, void* const* events, int32_t count) {
+    if (!h) return SPMM_ERR_NULL_POINTER;
+    if (count < 0 || count > 8) return fail(h, SPMM_ERR_INVALID_ARG, "timing event count must be in [0, 8]");
+    if (count > 0 && !events) return fail(h, SPMM_ERR_NULL_POINTER, "events is NULL");
+    for (int i = 0; i < 8; ++i) h->ev[i] = (i < count) ? static_cast<cudaEvent_t>(events[i]) : nullptr;
+    h->nev = count;
+    return SPMM_OK;
+}
+
+spmm_status spmm_merge_partition(const int32_t* row_offsets, int64_t m, int64_t nnz, int32_t items_per_cta,
+                                 int32_t partition, int64_t num_ctas, int32_t* states_out, void* stream) {
+    if (!states_out || (m > 0 && !row_offsets)) return SPMM_ERR_NULL_POINTER;
+    if (partition != SPMM_PARTITION_MERGE_PATH && partition != SPMM_PARTITION_NONZERO_SPLIT) return SPMM_ERR_INVALID_ARG;
+    if (items_per_cta <= 0 || m < 0 || nnz < 0 || m + nnz >= 0x7fffffffLL) return SPMM_ERR_INVALID_ARG;
+    if (num_ctas != spmm_merge_num_ctas(m, nnz, items_per_cta, partition)) return SPMM_ERR_INVALID_ARG;
+    if (num_ctas == 0) return SPMM_OK;
+    const long long pgrid = (num_ctas + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
+    k_partition<<<(unsigned)pgrid, THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+        row_offsets, (int)m, (int)nnz, items_per_cta, partition, (int)num_ctas, states_out);
+    return cudaGetLastError() == cudaSuccess ? SPMM_OK : SPMM_ERR_CUDA;
+}
+
+spmm_status spmm_partition_rows(const int32_t* host_row_offsets, int64_t m, int32_t parts, int32_t mode,
+                                int64_t* row_bounds) {
+    if (!row_bounds || (m > 0 && !host_row_offsets)) return SPMM_ERR_NULL_POINTER;
+    if (parts < 1 || m < 0 || (mode != 0 && mode != 1)) return SPMM_ERR_INVALID_ARG;
+    const int64_t nnz = m > 0 ? host_row_offsets[m] : 0;
+    row_bounds[0] = 0;
+    for (int p = 1; p < parts; ++p) {
+        int64_t b;
+        if (mode == 0) {
+            // nnz-balanced: first row r with ro[r] >= p*nnz/parts (lower_bound)
+            const long double target = (long double)nnz * p / parts;
+            int64_t lo = 0, hi = m;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) / 2;
+                if ((long double)host_row_offsets[mid] < target) lo = mid + 1; else hi = mid;
+            }
+            b = lo;
+        } else {
+            // merge-path balanced: row coordinate of diagonal D = p*(m+nnz)/parts
+            const int64_t D = (int64_t)((long double)(m + nnz) * p / parts);
+            int64_t lo = std::max<int64_t>(0, D - nnz), hi = std::min<int64_t>(D, m);
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) / 2;
+                if ((int64_t)host_row_offsets[mid + 1] <= D - mid - 1) lo = mid + 1; else hi = mid;
+            }
+            b = lo;
+        }
+        row_bounds[p] = std::max(b, row_bounds[p - 1]);
+    }
+    row_bounds[parts] = m;
+    for (int p = 1; p < parts; ++p) row_bounds[p] = std::min(row_bounds[p], m);
+    return SPMM_OK;
+}
+
+}  // extern "C"

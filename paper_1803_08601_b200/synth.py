@@ -138,17 +138,19 @@ def from_lengths_unsorted(m: int, k: int, lengths: list[int], seed: int, allow_d
             keys = counter_u32(seed, 8, i * k + _arange(k, "cpu"))
             sel = torch.argsort(keys * k + _arange(k, "cpu"))[:L]
             out.append(torch.sort(sel)[0])
-        else:
+        else:  # draw candidates in batches, keep first occurrences in draw order
             got: list[int] = []
             seen = set()
             t = 0
             while len(got) < L:
-                h = int(counter_u32(seed, 9, torch.tensor([i * 1_000_003 + t], dtype=torch.int64))[0])
-                c = (h * k) >> 32
-                t += 1
-                if c not in seen:
-                    seen.add(c)
-                    got.append(c)
+                cand = ((counter_u32(seed, 9, i * 1_000_003 + t + _arange(4 * L, "cpu")) * k) >> 32).tolist()
+                t += 4 * L
+                for c in cand:
+                    if c not in seen:
+                        seen.add(c)
+                        got.append(c)
+                        if len(got) == L:
+                            break
             out.append(torch.tensor(sorted(got), dtype=torch.int64))
     cols = torch.cat(out).to(torch.int32) if out else torch.zeros(0, dtype=torch.int32)
     return CsrPattern(m, k, ro.to(torch.int32).to(device), cols.to(device), name)
@@ -157,16 +159,20 @@ def from_lengths_unsorted(m: int, k: int, lengths: list[int], seed: int, allow_d
 # ----------------------------------------------------------------------------------------------
 # structure generators
 # ----------------------------------------------------------------------------------------------
-def banded(m: int, lo: int = 8, hi: int = 7, device="cpu") -> CsrPattern:
-    """Circulant band: row i has columns {(i+o) mod m : o in [-lo, hi]}, sorted (SURVEY.md §8(d) cfg 2)."""
+def banded(m: int, lo: int = 8, hi: int = 7, device="cpu", row_begin: int = 0, row_end: int | None = None
+           ) -> CsrPattern:
+    """Circulant band: row i has columns {(i+o) mod m : o in [-lo, hi]}, sorted (SURVEY.md §8(d) cfg 2).
+    row_begin/row_end select a row block (rows keep their global column indices; k stays m)."""
     w = lo + hi + 1
     assert w <= m
-    i = _arange(m, device)
+    row_end = m if row_end is None else row_end
+    i = _arange(row_end - row_begin, device) + row_begin
     offs = torch.arange(-lo, hi + 1, dtype=torch.int64, device=device)
     cols = torch.remainder(i[:, None] + offs[None, :], m)
     cols = torch.sort(cols, dim=1)[0]
-    ro = (_arange(m + 1, device) * w).to(torch.int32)
-    return CsrPattern(m, m, ro, cols.reshape(-1).to(torch.int32).contiguous(), f"banded_m{m}_w{w}")
+    rows = row_end - row_begin
+    ro = (_arange(rows + 1, device) * w).to(torch.int32)
+    return CsrPattern(rows, m, ro, cols.reshape(-1).to(torch.int32).contiguous(), f"banded_m{m}_w{w}")
 
 
 def uniform_rows(m: int, k: int, d: int, seed: int, device="cpu") -> CsrPattern:
@@ -297,8 +303,9 @@ def _vals(kind: str, h: torch.Tensor) -> torch.Tensor:
     raise ValueError(kind)
 
 
-def values(nnz: int, seed: int, kind: str, device="cpu") -> torch.Tensor:
-    return _vals(kind, counter_u32(seed, 30, _arange(nnz, device)))
+def values(nnz: int, seed: int, kind: str, device="cpu", offset: int = 0) -> torch.Tensor:
+    """Values of nonzeros offset .. offset+nnz-1 (offset = global position of a row block)."""
+    return _vals(kind, counter_u32(seed, 30, _arange(nnz, device) + offset))
 
 
 def dense(rows: int, n: int, seed: int, kind: str, ld: int | None = None, device="cpu",

@@ -1,0 +1,342 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI (ctypes binding), against the CPU
+oracle on the same seeded inputs.  Bar (north_star / SURVEY.md §8(c)): bit-exact for int32
+plus-times and both min-plus semirings; |C - C_ref| <= 1e-5 * (|A|.|B|)_ij for fp32 plus-times.
+Integer-valued partition outputs are compared bit-exactly with the oracle's brute-force walk."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1803_08601_b200 import spmm as S
+from paper_1803_08601_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    S.load()
+
+
+def make_inputs(p: synth.CsrPattern, kind: str, n: int, seed: int = 7, ldb=None, ldc=None, b_offset=0):
+    val = synth.values(p.nnz, seed + 100, kind)
+    Bh = synth.dense(p.k, n, seed + 200, kind, ld=ldb)
+    ld_b = Bh.shape[1]
+    ro = p.row_offsets.to(DEV)
+    ci = p.col_indices.to(DEV)
+    vd = val.to(DEV)
+    if b_offset:  # misaligned B: shift the base pointer by b_offset elements
+        flat = torch.empty(Bh.numel() + b_offset, dtype=Bh.dtype, device=DEV)
+        flat[b_offset:] = Bh.reshape(-1).to(DEV)
+        Bd = flat[b_offset:].view(p.k, ld_b)
+    else:
+        Bd = Bh.to(DEV)
+    ld_c = n if ldc is None else ldc
+    poison = float("nan") if kind.startswith("f32") else -(2**31)
+    Cd = torch.full((p.m, ld_c), poison, dtype=Bh.dtype, device=DEV)
+    return val, Bh, ro, ci, vd, Bd, Cd
+
+
+def run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd, **plan_kw):
+    sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
+    op = S.CsrSpmm(ro, ci, vd, p.k)
+    chosen = op.plan(n, algo, sr, **plan_kw)
+    Cview = Cd[:, :n] if Cd.shape[1] > n else Cd
+    op.execute(Bd[:, :n] if Bd.shape[1] > n else Bd, Cview)
+    torch.cuda.synchronize()
+    info = op.info()
+    op.close()
+    return chosen, info
+
+
+def check(p, kind, n, val, Bh, Cd, rows=None, ldb=None):
+    C = Cd[:, :n].cpu().numpy()
+    if rows is not None:
+        C = C[np.asarray(rows)]
+    ref = oracle.spmm(kind, p.m, p.k, n, p.row_offsets, p.col_indices, val, Bh, ldb=Bh.shape[1], rows=rows)
+    if kind == "f32_plus_times":
+        Cref, bound = ref
+        ok, worst, idx = oracle.check_f32(C, Cref, bound, TOL)
+        assert ok, f"fp32 tolerance violated: worst |err|/bound = {worst} at flat index {idx}"
+    else:
+        if not np.array_equal(C, ref):
+            bad = np.argwhere(C != ref)
+            r, c = bad[0]
+            raise AssertionError(f"{len(bad)} mismatches, first at ({r},{c}): gpu {C[r, c]} ref {ref[r, c]}")
+    if Cd.shape[1] > n:  # columns [n, ldc) untouched
+        tail = Cd[:, n:].cpu()
+        if kind.startswith("f32"):
+            assert torch.isnan(tail).all()
+        else:
+            assert (tail == -(2**31)).all()
+
+
+ALGOS = ["rowsplit", "merge", "auto"]
+
+
+# ------------------------------------------------------------------------------------------------
+# config 0 (tiny uniform) across semirings, n and both kernels
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 8, 16, 31, 32, 33, 48, 64, 65, 100, 127, 128])
+@pytest.mark.parametrize("algo", ALGOS)
+def test_config0_parity(kind, n, algo):
+    p = synth.config_pattern(0)
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd)
+    check(p, kind, n, val, Bh, Cd)
+
+
+@pytest.mark.parametrize("partition", ["merge_path", "nonzero_split"])
+@pytest.mark.parametrize("items", [256, 512, 2048, 16384])
+@pytest.mark.parametrize("kind", ["f32_plus_times", "i32_min_plus"])
+def test_merge_partitions_and_tile_sizes(partition, items, kind):
+    p = synth.lognormal_rows(3000, 2000, 7.92, 17)  # ragged rows, empty rows, several CTAs
+    n = 64
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    run_gpu(p, kind, n, "merge", ro, ci, vd, Bd, Cd, partition=partition, items_per_cta=items)
+    check(p, kind, n, val, Bh, Cd)
+
+
+# ------------------------------------------------------------------------------------------------
+# adversarial families (SPEC.md:457 / SURVEY.md §4)
+# ------------------------------------------------------------------------------------------------
+def _families():
+    fam = {}
+    fam["all_empty"] = synth.from_rows(50, 40, [[] for _ in range(50)])
+    fam["one_giant_row"] = synth.explicit_lengths(1, 200_000, [100_000], seed=3)
+    fam["giant_row_plus_singletons"] = synth.explicit_lengths(1001, 150_000, [100_000] + [1] * 1000, seed=4)
+    fam["lengths_1_31_32_33"] = synth.explicit_lengths(400, 300, [1, 31, 32, 33] * 100, seed=5)
+    lens = [0] * 997 + [5, 0, 0, 64]
+    fam["many_empty_rows"] = synth.explicit_lengths(len(lens), 100, lens, seed=6)
+    fam["leading_trailing_empty"] = synth.explicit_lengths(12, 10, [0, 0, 0, 3, 0, 10, 1, 0, 0, 2, 0, 0], seed=7)
+    fam["unsorted_duplicates"] = synth.from_lengths_unsorted(300, 50, [int(x) for x in (np.arange(300) % 13)],
+                                                             seed=8, allow_dups=True)
+    fam["rmat12"] = synth.rmat(12, 16, 99)
+    fam["aspect_short_wide"] = synth.aspect(1 << 16, 4)      # 4 rows x 16384 nnz
+    fam["aspect_tall"] = synth.aspect(1 << 16, 1 << 15)      # 32768 rows x 2
+    fam["single_row_single_nnz"] = synth.from_rows(1, 1, [[0]])
+    return fam
+
+
+FAMILY_NAMES = ["all_empty", "one_giant_row", "giant_row_plus_singletons", "lengths_1_31_32_33", "many_empty_rows",
+                "leading_trailing_empty", "unsorted_duplicates", "rmat12", "aspect_short_wide", "aspect_tall",
+                "single_row_single_nnz"]
+_FAM_CACHE = {}
+
+
+def family(name):
+    if not _FAM_CACHE:
+        _FAM_CACHE.update(_families())
+    return _FAM_CACHE[name]
+
+
+@pytest.mark.parametrize("fam", FAMILY_NAMES)
+@pytest.mark.parametrize("kind", ["f32_plus_times", "i32_plus_times", "f32_min_plus"])
+@pytest.mark.parametrize("n", [1, 16, 33, 64, 128])
+@pytest.mark.parametrize("algo", ["rowsplit", "merge"])
+def test_adversarial_parity(fam, kind, n, algo):
+    p = family(fam)
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd)
+    check(p, kind, n, val, Bh, Cd)
+
+
+@pytest.mark.parametrize("algo", ["rowsplit", "merge"])
+@pytest.mark.parametrize("kind", synth.KINDS)
+def test_padding_and_misalignment(algo, kind):
+    """ldb/ldc > n (poisoned padding must not be read or written) and a B base pointer that is
+    only 4-byte aligned (forces the scalar path)."""
+    p = synth.uniform_rows(700, 500, 9, 21)
+    for n, ldb, ldc, off in ((64, 70, 72, 0), (64, 64, 64, 1), (17, 20, 19, 3), (128, 131, 128, 1), (1, 3, 2, 0)):
+        val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, ldb=ldb, ldc=ldc, b_offset=off)
+        run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd)
+        check(p, kind, n, val, Bh, Cd)
+
+
+def test_integer_and_minplus_bit_identical_across_kernels():
+    """Order-independent semirings: every kernel / partition / tile size gives the same bits."""
+    p = synth.rmat(13, 8, 5)
+    for kind in ("i32_plus_times", "i32_min_plus", "f32_min_plus"):
+        outs = []
+        for algo, kw in (("rowsplit", {}), ("merge", {}), ("merge", {"partition": "nonzero_split"}),
+                         ("merge", {"items_per_cta": 256}), ("auto", {})):
+            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, 64)
+            run_gpu(p, kind, 64, algo, ro, ci, vd, Bd, Cd, **kw)
+            outs.append(Cd.cpu())
+        for o in outs[1:]:
+            assert torch.equal(o, outs[0])
+
+
+def test_fp32_deterministic_run_to_run():
+    p = synth.rmat(12, 16, 8)
+    for algo in ("rowsplit", "merge"):
+        res = []
+        for _ in range(2):
+            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, "f32_plus_times", 64)
+            run_gpu(p, "f32_plus_times", 64, algo, ro, ci, vd, Bd, Cd)
+            res.append(Cd.cpu())
+        assert torch.equal(res[0], res[1])
+
+
+def test_row_permutation_equivariance_and_power_of_two_scaling():
+    p = synth.uniform_rows(513, 400, 11, 33)
+    kind, n = "f32_plus_times", 32
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    run_gpu(p, kind, n, "rowsplit", ro, ci, vd, Bd, Cd)
+    base = Cd.cpu()
+    perm = torch.randperm(p.m, generator=torch.Generator().manual_seed(1))
+    lens = (p.row_offsets[1:] - p.row_offsets[:-1]).long()
+    starts = p.row_offsets[:-1].long()
+    new_ro = torch.zeros(p.m + 1, dtype=torch.int64)
+    new_ro[1:] = torch.cumsum(lens[perm], 0)
+    idx = torch.cat([torch.arange(starts[r], starts[r] + lens[r]) for r in perm.tolist()])
+    Cd2 = torch.empty_like(Cd)
+    op = S.CsrSpmm(new_ro.to(torch.int32).to(DEV), p.col_indices[idx].to(DEV), (val[idx] * 8.0).to(DEV), p.k)
+    op.plan(n, "rowsplit")
+    op.execute(Bd, Cd2)
+    torch.cuda.synchronize()
+    assert torch.equal(Cd2.cpu(), base[perm] * 8.0)
+
+
+# ------------------------------------------------------------------------------------------------
+# partition kernel (Alg. 1 line 2) vs the oracle's brute-force walk / linear scan, bit-exact
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [0, 1])
+def test_partition_kernel_matches_oracle(mode):
+    rng = np.random.default_rng(40 + mode)
+    cases = [np.array([0, 2, 2, 5, 6], np.int32), np.array([0, 0, 0, 0], np.int32)]
+    for _ in range(60):
+        m = int(rng.integers(1, 3000))
+        lens = rng.integers(0, 12, m)
+        lens[rng.random(m) < 0.5] = 0
+        if rng.random() < 0.2:
+            lens[int(rng.integers(0, m))] = int(rng.integers(100, 5000))
+        ro = np.zeros(m + 1, np.int32)
+        ro[1:] = np.cumsum(lens)
+        cases.append(ro)
+    for ro in cases:
+        m, nnz = len(ro) - 1, int(ro[-1])
+        for items in (1, 3, 7, 256, 2048):
+            nc = S.spmm_merge_num_ctas(m, nnz, items, mode)
+            if nc <= 0:
+                continue
+            states = torch.empty(2 * (nc + 1), dtype=torch.int32, device=DEV)
+            rod = torch.from_numpy(ro).to(DEV)
+            st = S.spmm_merge_partition(rod.data_ptr(), m, nnz, items, mode, nc, states.data_ptr())
+            assert st == S.SPMM_OK
+            torch.cuda.synchronize()
+            got = states.cpu().numpy().reshape(-1, 2)
+            if mode == 0:
+                diags = np.minimum(np.arange(nc + 1, dtype=np.int64) * items, m + nnz)
+                wi, wj = oracle.merge_path_walk(ro, diags)
+                assert np.array_equal(got[:, 0], wi) and np.array_equal(got[:, 1], wj)
+            else:
+                rows = oracle.nonzero_split(ro, items, nc)
+                assert np.array_equal(got[:nc, 0], rows)
+                assert np.array_equal(got[:nc, 1], np.arange(nc) * items)
+                assert tuple(got[nc]) == (m, nnz)
+    # SPEC.md:284 worked example through the kernel
+    ro = torch.tensor([0, 2, 2, 5, 6], dtype=torch.int32, device=DEV)
+    states = torch.empty(2 * 3, dtype=torch.int32, device=DEV)
+    assert S.spmm_merge_partition(ro.data_ptr(), 4, 6, 3, 1, 2, states.data_ptr()) == S.SPMM_OK
+    assert states.cpu().view(-1, 2)[:, 0].tolist() == [0, 2, 4]
+
+
+# ------------------------------------------------------------------------------------------------
+# heuristic (§5.4) and the ABI's error behaviour on a live device
+# ------------------------------------------------------------------------------------------------
+def test_heuristic_choice_matches_oracle_rule():
+    for d in (1, 2, 7, 9, 10, 16, 62):
+        p = synth.uniform_rows(2000, 4000, d, d)
+        vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
+        op = S.CsrSpmm(p.row_offsets.to(DEV), p.col_indices.to(DEV), vd, p.k)
+        chosen = op.plan(64, "auto", policy="paper")
+        assert chosen == oracle.heuristic(oracle.mean_row_length(p.nnz, p.m))
+        op.close()
+    # skew guard (AUTO policy): R-MAT has d >= 9.35 but a row far above the per-warp fair share
+    r = synth.rmat(16, 16, 1805)
+    vd = synth.values(r.nnz, 1, "f32_plus_times").to(DEV)
+    op = S.CsrSpmm(r.row_offsets.to(DEV), r.col_indices.to(DEV), vd, r.k)
+    assert op.plan(64, "auto", policy="paper") == "rowsplit"
+    assert op.plan(64, "auto", policy="auto") == "merge"
+    assert op.info()["max_row_length"] == int((r.row_offsets[1:] - r.row_offsets[:-1]).max())
+    op.close()
+
+
+def test_abi_errors_on_device():
+    p = synth.uniform_rows(100, 100, 4, 2)
+    vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
+    op = S.CsrSpmm(p.row_offsets.to(DEV), p.col_indices.to(DEV), vd, p.k)
+    with pytest.raises(S.SpmmError) as e:
+        op.plan(129)
+    assert e.value.status == S.SPMM_ERR_UNSUPPORTED
+    st = S.spmm_csr_execute(op._h, None, 8, None, 8, 8, None, 0)
+    assert st == S.SPMM_ERR_NOT_PLANNED
+    op.plan(8, "merge")
+    B = torch.zeros(100, 8, device=DEV)
+    C = torch.zeros(100, 8, device=DEV)
+    assert S.spmm_csr_execute(op._h, B.data_ptr(), 8, C.data_ptr(), 8, 9, None, 0) == S.SPMM_ERR_INVALID_ARG
+    assert S.spmm_csr_execute(op._h, B.data_ptr(), 8, C.data_ptr(), 8, 8, op.workspace.data_ptr(), 0) == \
+        S.SPMM_ERR_WORKSPACE_TOO_SMALL
+    assert S.spmm_csr_execute(op._h, B.data_ptr(), 4, C.data_ptr(), 8, 8, op.workspace.data_ptr(),
+                              op.ws_bytes) == S.SPMM_ERR_INVALID_ARG
+    assert "workspace" in S.spmm_csr_last_error(op._h) or "ld" in S.spmm_csr_last_error(op._h)
+    op.close()
+    # validation catches broken CSR invariants
+    bad_ro = torch.tensor([0, 3, 2, 4], dtype=torch.int32, device=DEV)
+    col = torch.tensor([0, 1, 2, 3], dtype=torch.int32, device=DEV)
+    with pytest.raises(S.SpmmError) as e:
+        S.CsrSpmm(bad_ro, col, torch.ones(4, device=DEV), 4, validate=True)
+    assert e.value.status == S.SPMM_ERR_INVALID_CSR
+    good_ro = torch.tensor([0, 1, 2, 4], dtype=torch.int32, device=DEV)
+    with pytest.raises(S.SpmmError):
+        S.CsrSpmm(good_ro, torch.tensor([0, 1, 2, 9], dtype=torch.int32, device=DEV), torch.ones(4, device=DEV), 4,
+                  validate=True)
+    S.CsrSpmm(good_ro, col, torch.ones(4, device=DEV), 4, validate=True).close()
+
+
+def test_empty_and_degenerate_shapes():
+    # m = 0: no-op
+    ro = torch.zeros(1, dtype=torch.int32, device=DEV)
+    op = S.CsrSpmm(ro, torch.zeros(0, dtype=torch.int32, device=DEV), torch.zeros(0, device=DEV), 5)
+    op.plan(4)
+    op.execute(torch.zeros(5, 4, device=DEV), torch.zeros(0, 4, device=DEV))
+    op.close()
+    # nnz = 0: identity everywhere, for every semiring and both kernels
+    for kind in synth.KINDS:
+        p = synth.from_rows(9, 3, [[]] * 9)
+        for algo in ("rowsplit", "merge"):
+            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, 5)
+            run_gpu(p, kind, 5, algo, ro, ci, vd, Bd, Cd)
+            check(p, kind, 5, val, Bh, Cd)
+
+
+# ------------------------------------------------------------------------------------------------
+# BASELINE.json full sizes, in the launch configuration bench.py times, sampled rows
+# ------------------------------------------------------------------------------------------------
+def _sample_rows(p, extra_rows=(), seed=0):
+    lens = (p.row_offsets[1:] - p.row_offsets[:-1]).to(torch.int64)
+    longest = torch.topk(lens, min(256, p.m)).indices
+    rng = torch.Generator().manual_seed(seed)
+    rand = torch.randint(0, p.m, (4096,), generator=rng)
+    edge = torch.tensor([0, 1, p.m - 2, p.m - 1] + list(extra_rows), dtype=torch.int64).clamp(0, p.m - 1)
+    return torch.unique(torch.cat([longest.cpu(), rand, edge])).numpy()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("algo", ["auto", "rowsplit", "merge"])
+def test_full_size_configs_sampled(cfg, algo):
+    p = synth.config_pattern(cfg, device=DEV).to("cpu")
+    kind, n = "f32_plus_times", 64
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, seed=synth.STRUCT_SEED + cfg)
+    chosen, info = run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd)
+    rows = _sample_rows(p)
+    check(p, kind, n, val, Bh, Cd, rows=rows)
+    # every row was written (no poison left anywhere)
+    assert not torch.isnan(Cd).any()
