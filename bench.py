@@ -284,6 +284,10 @@ def main():
 
     # timed region: K steps, per-step CUDA events recorded by the library around each kernel
     evsets = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    for evs in evsets:  # torch creates the CUDA event lazily on first record: force creation
+        for e in evs:
+            e.record()
+    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     sampler.start()

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspmm.so")
 SOURCES = [os.path.join(CSRC, "spmm_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "rowsplit.cuh", "merge.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "ptx.cuh", "tile.cuh", "merge.cuh")] + \
     [os.path.join(ROOT, "include", "spmm.h")]
 
 NVCC_FLAGS = [
@@ -35,18 +35,26 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libspmm.so (or a variant at `out` with extra -D defines, for tuning experiments)."""
+    lib = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES]
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", lib + ".tmp", *SOURCES]
     if verbose:
         cmd += ["-Xptxas", "-v"]
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, defines=a.D))

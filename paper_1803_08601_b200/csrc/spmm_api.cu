@@ -12,7 +12,7 @@
 #include "../../include/spmm.h"
 #include "common.cuh"
 #include "merge.cuh"
-#include "rowsplit.cuh"
+#include "tile.cuh"
 
 using namespace spmm;
 
@@ -32,7 +32,8 @@ struct spmm_csr_s {
     int64_t max_row = -1;
     int64_t num_ctas = 0;
     int32_t items = 2048;
-    int32_t rounds = 4;
+    int32_t rows_per_tile = 128;  // row split: rows per tile
+    int32_t capz = 4104;          // row split: staged nonzeros per tile (+8 slack)
     size_t ws_bytes = 0;
     int* d_scratch = nullptr;  // 16 bytes: plan-time reduction / validation flags
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
@@ -44,8 +45,14 @@ namespace {
 
 constexpr int kDefaultItems = 2048;
 constexpr int kNumSMs = 148;
-constexpr int kRowsplitU = 8;
-constexpr int kMergeU = 8;
+#ifndef RS_U
+#define RS_U 8
+#endif
+#ifndef MG_U
+#define MG_U 16
+#endif
+constexpr int kRowsplitU = RS_U;
+constexpr int kMergeU = MG_U;
 
 spmm_status fail(spmm_csr_t h, spmm_status s, const std::string& msg) {
     if (h) h->err = msg;
@@ -114,9 +121,12 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
     if (folded) {
         c.G = std::min(32, pow2ceil(lanes));
         c.NV = (lanes + 31) / 32;
-    } else {
+    } else {  // one worker per warp: narrowest vector that covers n with 32 lanes
+        const int want = n <= 32 ? 1 : (n <= 64 ? 2 : 4);
+        if (want < vec) c.vec = want;
+        const int l2 = (n + c.vec - 1) / c.vec;
         c.G = 32;
-        c.NV = (lanes + 31) / 32;
+        c.NV = (l2 + 31) / 32;
     }
     return c;
 }
@@ -124,22 +134,42 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
 // ------------------------------------------------------------------------------------------------
 // dispatch tables
 // ------------------------------------------------------------------------------------------------
-template <typename T, int SR>
-cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, const T* B, long long ldb, T* C, long long ldc,
-                            cudaStream_t st) {
-    const int S = 32 / cfg.G;
-    const long long rows_per_cta = (long long)WARPS_PER_CTA * S * h->rounds;
-    const long long grid = (h->m + rows_per_cta - 1) / rows_per_cta;
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
+    }
+    return sms;
+}
+
+template <typename T, int SR, int MODE, int V, int G, int NV, int U>
+cudaError_t launch_tile(const TileParams& P, cudaStream_t st) {
+    auto kfn = k_tile<T, SR, MODE, V, G, NV, U>;
+    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n);
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, TE_THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm <= 0) return cudaErrorInvalidConfiguration;
+    const long long grid = std::min<long long>(P.num_ranges, (long long)per_sm * num_sms());
     if (grid <= 0) return cudaSuccess;
-    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    const int m = (int)h->m, n = h->n;
-    const T* val = static_cast<const T*>(h->val);
-#define RS_CASE(V, G_, NV_)                                                                                   \
-    case (V)*1000 + (G_)*10 + (NV_):                                                                          \
-        k_rowsplit<T, SR, V, G_, NV_, kRowsplitU><<<(unsigned)grid, THREADS, 0, st>>>(m, n, h->ro, h->col, val, \
-                                                                                     B, ldb, C, ldc, h->rounds); \
-        break;
+    kfn<<<(unsigned)grid, TE_THREADS, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+template <typename T, int SR>
+cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaStream_t st) {
+    P.num_ranges = (int)((h->m + h->rows_per_tile - 1) / h->rows_per_tile);
+    P.rows_per_tile = h->rows_per_tile;
+    P.capr = h->rows_per_tile + 8;
+    P.capz = h->capz;
     mark(h, 0, st);
+    cudaError_t e;
+#define RS_CASE(V, G_, NV_) \
+    case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kRowsplitU>(P, st); break;
     switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
         RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 16, 1) RS_CASE(4, 32, 1)
         RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 16, 1) RS_CASE(2, 32, 1)
@@ -150,12 +180,11 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, const T* B, long lo
     }
 #undef RS_CASE
     mark(h, 1, st);
-    return cudaGetLastError();
+    return e;
 }
 
 template <typename T, int SR>
-cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, const T* B, long long ldb, T* C, long long ldc,
-                         unsigned char* ws, cudaStream_t st) {
+cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned char* ws, cudaStream_t st) {
     const long long NC = h->num_ctas;
     if (NC <= 0) return cudaSuccess;
     int* states = reinterpret_cast<int*>(ws);
@@ -165,39 +194,37 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, const T* B, long long 
     int* carry_flag = reinterpret_cast<int*>(ws + off);
     off += align256(sizeof(int) * NC);
     T* carry_val = reinterpret_cast<T*>(ws + off);
-    const int m = (int)h->m, n = h->n, nnz = (int)h->nnz, items = h->items;
+    const int items = h->items;
     // phase 1: PartitionSpmm (Alg. 1 line 2)
     const long long pgrid = (NC + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     mark(h, 0, st);
-    k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, m, nnz, items, h->opts.partition, (int)NC, states);
+    k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, (int)h->m, (int)h->nnz, items, h->opts.partition, (int)NC,
+                                                     states);
     mark(h, 1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // phase 2: per-CTA compute + carry-out (Alg. 1 lines 3-23)
-    const size_t smem = merge_smem_bytes(items, n, (int)sizeof(T));
-    const T* val = static_cast<const T*>(h->val);
-#define MG_CASE(V, NV_)                                                                                  \
-    case (V)*10 + (NV_): {                                                                               \
-        auto kfn = k_merge<T, SR, V, NV_, kMergeU>;                                                       \
-        if (smem > 48 * 1024) {                                                                          \
-            e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-            if (e != cudaSuccess) return e;                                                              \
-        }                                                                                                \
-        kfn<<<(unsigned)NC, THREADS, smem, st>>>(m, n, nnz, h->ro, h->col, val, B, ldb, C, ldc, states, items, \
-                                                 carry_row, carry_flag, carry_val);                      \
-        break;                                                                                           \
-    }
+    P.num_ranges = (int)NC;
+    P.states = states;
+    P.items = items;
+    P.carry_row = carry_row;
+    P.carry_flag = carry_flag;
+    P.carry_val = carry_val;
+    P.capr = items + 8;
+    P.capz = items + 8;
+#define MG_CASE(V, NV_) \
+    case (V)*10 + (NV_): e = launch_tile<T, SR, MODE_MERGE, V, 32, NV_, kMergeU>(P, st); break;
     switch (cfg.vec * 10 + cfg.NV) {
         MG_CASE(4, 1) MG_CASE(2, 1) MG_CASE(2, 2) MG_CASE(1, 1) MG_CASE(1, 2) MG_CASE(1, 3) MG_CASE(1, 4)
         default: return cudaErrorNotSupported;
     }
 #undef MG_CASE
     mark(h, 2, st);
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     // phase 3: FixCarryOut (Alg. 1 line 24)
     const long long fgrid = (NC + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-    k_fixup<T, SR><<<(unsigned)fgrid, THREADS, 0, st>>>((int)NC, n, carry_row, carry_flag, carry_val, C, ldc);
+    k_fixup<T, SR><<<(unsigned)fgrid, THREADS, 0, st>>>((int)NC, h->n, carry_row, carry_flag, carry_val,
+                                                        static_cast<T*>(P.C), P.ldc);
     mark(h, 3, st);
     return cudaGetLastError();
 }
@@ -205,12 +232,25 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, const T* B, long long 
 template <typename T, int SR>
 cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, long long ldc, void* ws,
                 cudaStream_t st) {
-    const T* B = static_cast<const T*>(Bv);
-    T* C = static_cast<T*>(Cv);
+    TileParams P{};
+    P.m = (int)h->m;
+    P.n = h->n;
+    P.nnz = (int)h->nnz;
+    P.ro = h->ro;
+    P.col = h->col;
+    P.val = h->val;
+    P.B = Bv;
+    P.ldb_bytes = (unsigned)(ldb * (long long)sizeof(T));
+    P.C = Cv;
+    P.ldc = ldc;
+#ifndef PF_OFF
+    // L2 prefetch of gathered B rows: needs 16B-aligned rows; prefetch whole 16-byte granules only
+    if (((uintptr_t)Bv % 16) == 0 && (P.ldb_bytes % 16) == 0 && h->n * sizeof(T) >= 16)
+        P.pf_bytes = (unsigned)((h->n * sizeof(T)) & ~(size_t)15);
+#endif
     if (h->chosen == SPMM_ALGO_ROWSPLIT)
-        return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), B, ldb, C, ldc, st);
-    return launch_merge<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, false), B, ldb, C, ldc,
-                               static_cast<unsigned char*>(ws), st);
+        return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), P, st);
+    return launch_merge<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, false), P, static_cast<unsigned char*>(ws), st);
 }
 
 }  // namespace
@@ -318,8 +358,8 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     if (o.partition != SPMM_PARTITION_MERGE_PATH && o.partition != SPMM_PARTITION_NONZERO_SPLIT)
         return fail(h, SPMM_ERR_INVALID_ARG, "bad partition");
     int items = o.items_per_cta ? o.items_per_cta : kDefaultItems;
-    if (items < 256 || items > 16384 || items % 256 != 0)
-        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 256 in [256, 16384]");
+    if (items < 256 || items > 8192 || items % 256 != 0)
+        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 256 in [256, 8192]");
     o.items_per_cta = items;
     h->threshold = threshold > 0 ? threshold : 9.35;
     h->n = n;
@@ -363,9 +403,16 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
                           align256(elem * (size_t)NC * n);
         }
     } else {
-        const int S = 32 / std::min(32, pow2ceil((n + 3) / 4));
-        const long long rpc = (long long)WARPS_PER_CTA * S * h->rounds;
-        h->num_ctas = (h->m + rpc - 1) / rpc;
+        // row tiles of R rows sized so a typical tile's nonzeros fit the staged shared-memory slice
+        const double dd = std::max(1.0, d);
+        int R = 1;
+        while (R * 2 <= 4096 && R * 2 * dd <= 2048.0) R *= 2;
+        R = std::max(16, std::min(R, 1024));
+        h->rows_per_tile = R;
+        long long z = (long long)std::ceil(2.0 * R * dd);
+        z = std::max<long long>(1024, std::min<long long>(z, 8192));
+        h->capz = (int)(((z + 3) & ~3LL) + 8);
+        h->num_ctas = (h->m + R - 1) / R;
     }
     h->planned = true;
     if (workspace_bytes) *workspace_bytes = h->ws_bytes;
@@ -408,7 +455,7 @@ spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, 
     if (h->ws_bytes > 0 && !workspace) return fail(h, SPMM_ERR_NULL_POINTER, "workspace is NULL");
     if (h->ws_bytes > 0 && ((uintptr_t)workspace % 16) != 0)
         return fail(h, SPMM_ERR_INVALID_ARG, "workspace must be 16-byte aligned");
-    if ((long long)h->m * ldc >= (1LL << 40) || (long long)h->k * ldb >= (1LL << 40))
+    if ((long long)h->m * ldc >= (1LL << 40) || (long long)h->k * ldb >= (1LL << 40) || ldb >= (1LL << 29))
         return fail(h, SPMM_ERR_UNSUPPORTED, "matrix too large");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e;

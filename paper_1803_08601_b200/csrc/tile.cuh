@@ -1,0 +1,588 @@
+// tile.cuh -- the sm_100a compute kernel shared by both of the paper's algorithms: a persistent,
+// warp-specialised "tile engine".
+//
+//   warp 8 (producer, one elected lane issues): walks this CTA's tiles, computes each tile's bounds
+//     and stages the tile's slice of A -- row offsets, column indices, values -- into shared memory
+//     with 1-D TMA bulk copies (cp.async.bulk, L2 evict-first), double-buffered, completion on a
+//     transaction-count mbarrier.  This is the paper's GlobalToShared step (Alg. 1 line 5,
+//     PAPER.md:146), made asynchronous so the next tile streams in while this one is computed.
+//   warps 0..7 (consumers): read (col, val) pairs from shared memory as broadcasts (every lane of a
+//     row group needs the same pair: the role of the paper's 32 `__shfl` broadcast rounds,
+//     PAPER.md:122, Alg. 1 lines 14-17), gather B rows with lanes over columns (coalesced float4 /
+//     float2 loads of row-major B), U gathers in flight before the first FMA (ILP,
+//     PAPER.md:55-57), accumulate with packed FFMA2, and write finished rows of C with streaming stores.
+//
+// MODE_ROWSPLIT (Algorithm I, §4.1): a tile is a fixed block of rows; each row is owned by one group
+//   of G lanes (G = ceil(n/VEC) rounded to a power of two, so a warp runs 32/G rows); no carries.
+// MODE_MERGE (Algorithm II, §4.2): a tile is one CTA range of the merge-path partition (k_partition,
+//   Alg. 1 line 2); each warp takes an equal share of the tile's items (rows + nonzeros) by a second
+//   merge-path search in shared memory and streams them; carry-outs are resolved in the CTA and the
+//   CTA's open row goes to the global carry array for k_fixup (Alg. 1 lines 22-24).
+#pragma once
+#include <type_traits>
+
+#include "common.cuh"
+#include "merge.cuh"
+#include "ptx.cuh"
+
+namespace spmm {
+
+constexpr int TE_CWARPS = 8;                    // consumer warps
+constexpr int TE_THREADS = 32 * (TE_CWARPS + 1);  // + 1 producer warp
+constexpr int TE_CONSUMERS = 32 * TE_CWARPS;
+#ifndef TE_STAGES_DEF
+#define TE_STAGES_DEF 3
+#endif
+#ifndef TE_MINB
+#define TE_MINB 2  // CTAs per SM the register allocation targets (__launch_bounds__)
+#endif
+constexpr int TE_STAGES = TE_STAGES_DEF;        // shared-memory pipeline depth (tiles in flight)
+enum : int { MODE_ROWSPLIT = 0, MODE_MERGE = 1 };
+
+struct TileParams {
+    int m, n, nnz;
+    const int* ro;
+    const int* col;
+    const void* val;
+    const void* B;
+    unsigned ldb_bytes;  // ldb * sizeof(T) (< 2^32)
+    void* C;
+    long long ldc;
+    int num_ranges;     // rowsplit: row tiles; merge: partition CTAs
+    int rows_per_tile;  // rowsplit
+    const int* states;  // merge: (row, nz) per range boundary
+    int items;          // merge: items per sub-tile (shared-memory capacity)
+    int* carry_row;
+    int* carry_flag;
+    void* carry_val;
+    int capr, capz;     // elements per buffer: row offsets / (col, val)
+    unsigned pf_bytes;  // bytes of each B row to prefetch into L2 ahead of the consumers (0 = off)
+};
+
+// tile descriptor written by the producer next to the staged data
+struct TileInfo {
+    int rs, zs, re, ze;  // merge-path state at tile start / end (rowsplit: zs = ro[rs], ze = ro[re])
+    int ebase, zbase;    // global index of E[0] and of COL[0]/VAL[0]
+    int range;           // partition range (merge) / row tile (rowsplit)
+    int flags;           // 1 first sub-tile of range, 2 last sub-tile, 4 staged, 8 done
+};
+
+__host__ __device__ inline size_t te_buf_bytes(int capr, int capz, int elem) {
+    return (size_t)capr * 4 + (size_t)capz * 4 + (size_t)capz * elem + 64;
+}
+__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n) {
+    return TE_STAGES * te_buf_bytes(capr, capz, elem) + 64 /*barriers*/ +
+           (size_t)(TE_CWARPS + 1) * n * elem + (size_t)(TE_CWARPS + 1) * 8 + 64;
+}
+
+// stage global src[begin, end) (4-byte elements, arr_len elements in the array) at dst; returns the
+// global index stored at dst[0] and adds TMA bytes to *tx.  Only the final partial 16-byte group of
+// the array is loaded with plain loads (never read past arr_len).
+__device__ __forceinline__ int te_stage(void* dst, const void* src, long long begin, long long end, long long arr_len,
+                                        uint64_t* bar, uint64_t pol, uint32_t* tx) {
+    const long long a_al = begin & ~3LL;
+    if (end <= begin) return (int)a_al;
+    long long b_al = (end + 3) & ~3LL;
+    const long long lim = arr_len & ~3LL;
+    if (b_al > lim) b_al = lim;
+    if (b_al > a_al) {
+        const uint32_t bytes = (uint32_t)((b_al - a_al) * 4);
+        tma_load_1d(dst, static_cast<const unsigned*>(src) + a_al, bytes, bar, pol);
+        *tx += bytes;
+    }
+    for (long long p = (b_al > begin ? b_al : begin); p < end; ++p)
+        static_cast<unsigned*>(dst)[p - a_al] = static_cast<const unsigned*>(src)[p];
+    return (int)a_al;
+}
+
+// predicated vector gather of B (no branch): o valid only if pred
+template <int VEC> __device__ __forceinline__ void ldg_pred(unsigned (&o)[VEC], const void* p, bool pred);
+template <> __device__ __forceinline__ void ldg_pred<1>(unsigned (&o)[1], const void* p, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; mov.b32 %0, 0; @q ld.global.nc.b32 %0, [%1];}"
+                 : "=r"(o[0]) : "l"(p), "r"((int)pred));
+}
+template <> __device__ __forceinline__ void ldg_pred<2>(unsigned (&o)[2], const void* p, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %3, 0; mov.b32 %0, 0; mov.b32 %1, 0; @q ld.global.nc.v2.b32 {%0, %1}, [%2];}"
+                 : "=r"(o[0]), "=r"(o[1]) : "l"(p), "r"((int)pred));
+}
+template <> __device__ __forceinline__ void ldg_pred<4>(unsigned (&o)[4], const void* p, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %5, 0; mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;"
+                 " @q ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];}"
+                 : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p), "r"((int)pred));
+}
+
+template <int VEC> __device__ __forceinline__ void ldg_nc(unsigned (&o)[VEC], const void* p) {
+    ldg_vec<VEC>(o, p);
+}
+
+// accumulator of VEC*NV columns for one lane
+template <typename T, int SR, int VEC, int NV> struct Acc {
+    T v[NV][VEC];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int a = 0; a < NV; ++a)
+#pragma unroll
+            for (int x = 0; x < VEC; ++x) v[a][x] = Ring<T, SR>::id();
+    }
+    __device__ __forceinline__ void mac(T a, const unsigned (&b)[NV][VEC]) {
+        if constexpr (std::is_same<T, float>::value && SR == SR_PLUS_TIMES && VEC % 2 == 0) {
+            const float2 aa = make_float2(a, a);
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+                for (int x = 0; x < VEC; x += 2) {
+                    float2 c = make_float2(v[q][x], v[q][x + 1]);
+                    c = ffma2(aa, make_float2(__uint_as_float(b[q][x]), __uint_as_float(b[q][x + 1])), c);
+                    v[q][x] = c.x;
+                    v[q][x + 1] = c.y;
+                }
+        } else {
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+#pragma unroll
+                for (int x = 0; x < VEC; ++x) v[q][x] = Ring<T, SR>::mac(v[q][x], a, from_bits<T>(b[q][x]));
+        }
+    }
+};
+
+template <typename T, int SR, int MODE, int VEC, int G, int NV, int U>
+__global__ void __launch_bounds__(TE_THREADS, TE_MINB)
+k_tile(const TileParams P) {
+    using R = Ring<T, SR>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int capr = P.capr, capz = P.capz, n = P.n, m = P.m;
+    const size_t bufb = te_buf_bytes(capr, capz, (int)sizeof(T));
+    auto E_of = [&](int b) { return reinterpret_cast<int*>(smem + b * bufb); };
+    auto COL_of = [&](int b) { return reinterpret_cast<int*>(smem + b * bufb + (size_t)capr * 4); };
+    auto VAL_of = [&](int b) { return reinterpret_cast<T*>(smem + b * bufb + (size_t)capr * 4 + (size_t)capz * 4); };
+    auto INFO_of = [&](int b) {
+        return reinterpret_cast<TileInfo*>(smem + b * bufb + (size_t)capr * 4 + (size_t)capz * (4 + sizeof(T)));
+    };
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + TE_STAGES * bufb);
+    uint64_t* empty = full + TE_STAGES;
+    T* Cw = reinterpret_cast<T*>(smem + TE_STAGES * bufb + 64);                 // [W+1][n] worker carries
+    int* Crow = reinterpret_cast<int*>(Cw + (size_t)(TE_CWARPS + 1) * n);  // [W+1]
+    int* Cflag = Crow + (TE_CWARPS + 1);                                 // [W+1]
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TE_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TE_CWARPS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // =============================== producer warp ===============================
+    if (warp == TE_CWARPS) {
+        const uint64_t pol = policy_evict_first();
+        int i = 0;
+        auto acquire = [&](int& b) {
+            b = i % TE_STAGES;
+            if (i >= TE_STAGES) mbar_wait(&empty[b], ((i / TE_STAGES) - 1) & 1);
+        };
+        // L2 prefetch of the B rows a staged tile will gather, when the tile's columns are clustered
+        // (banded / mesh-like matrices): one TMA bulk prefetch (cp.async.bulk.prefetch.L2) of the
+        // tile's B row span, issued once the tile's column indices have landed in shared memory, so
+        // the consumers' first-touch gathers hit L2 instead of paying a DRAM round trip.
+        auto prefetch_tile_b = [&](int pb, int ti) {
+            mbar_wait(&full[pb], (ti / TE_STAGES) & 1);
+            const TileInfo pi = *INFO_of(pb);
+            if (!(pi.flags & 4)) return;
+            const int cnt = pi.ze - pi.zs;
+            if (cnt <= 0) return;
+            const int* pc = COL_of(pb) + (pi.zs - pi.zbase);
+            int lo = 0x7fffffff, hi = -1;
+            for (int t = lane; t < cnt; t += 32) {
+                const int c = pc[t];
+                lo = min(lo, c);
+                hi = max(hi, c);
+            }
+            lo = __reduce_min_sync(FULL, lo);
+            hi = __reduce_max_sync(FULL, hi);
+            const long long span = (long long)hi - lo + 1;
+            if (span > 2LL * cnt) return;  // scattered columns: nothing compact to prefetch
+            const char* base = static_cast<const char*>(P.B) + (size_t)(unsigned)lo * P.ldb_bytes;
+            const long long bytes = (span - 1) * (long long)P.ldb_bytes + P.pf_bytes;
+            constexpr long long CHUNK = 16384;
+            for (long long off = (long long)lane * CHUNK; off < bytes; off += 32 * CHUNK) {
+                const long long len = min(CHUNK, bytes - off);
+                prefetch_l2_bulk(base + off, (uint32_t)(len & ~15LL));
+            }
+        };
+        for (int c = blockIdx.x; c < P.num_ranges; c += gridDim.x) {
+            long long rs, zs, re, ze;
+            if (MODE == MODE_ROWSPLIT) {
+                rs = (long long)c * P.rows_per_tile;
+                re = min((long long)m, rs + P.rows_per_tile);
+                zs = ld_stream(P.ro + rs);
+                ze = ld_stream(P.ro + re);
+            } else {
+                rs = P.states[2 * c];
+                zs = P.states[2 * c + 1];
+                re = P.states[2 * c + 2];
+                ze = P.states[2 * c + 3];
+            }
+            long long cr = rs, cz = zs;  // current sub-tile start
+            bool first = true;
+            while (true) {
+                long long nr = re, nz = ze;
+                if (MODE == MODE_MERGE && (re - cr) + (ze - cz) > P.items) {
+                    // oversize range (1-D nonzero split with many rows): cut at diagonal +items
+                    const long long D = cr + cz + P.items;
+                    const long long lo = max(cr, D - ze), hi = min(D - cz, re);
+                    nr = warp_search_first(lo, hi, MergePred{P.ro, D});
+                    nz = D - nr;
+                }
+                const bool last = (nr == re && nz == ze);
+                int b;
+                acquire(b);
+                if (lane == 0) {
+                    uint32_t tx = 0;
+                    TileInfo inf;
+                    inf.rs = (int)cr; inf.zs = (int)cz; inf.re = (int)nr; inf.ze = (int)nz;
+                    inf.range = c;
+                    bool staged;
+                    fence_proxy_async_smem();
+                    if (MODE == MODE_ROWSPLIT) {
+                        staged = (nz - cz) + 8 <= capz;
+                        inf.ebase = te_stage(E_of(b), P.ro, cr, nr + 1, (long long)m + 1, &full[b], pol, &tx);
+                    } else {
+                        staged = true;
+                        const long long e1 = min(nr + 1, (long long)m);  // row ends of rows cr..min(nr, m-1)
+                        inf.ebase = te_stage(E_of(b), P.ro, cr + 1, e1 + 1, (long long)m + 1, &full[b], pol, &tx);
+                    }
+                    if (staged) {
+                        inf.zbase = te_stage(COL_of(b), P.col, cz, nz, P.nnz, &full[b], pol, &tx);
+                        te_stage(VAL_of(b), P.val, cz, nz, P.nnz, &full[b], pol, &tx);
+                    } else {
+                        inf.zbase = 0;
+                    }
+                    inf.flags = (first ? 1 : 0) | (last ? 2 : 0) | (staged ? 4 : 0);
+                    *INFO_of(b) = inf;
+                    mbar_arrive_expect_tx(&full[b], tx);
+                }
+                __syncwarp();
+                if (P.pf_bytes && i >= 1) prefetch_tile_b((i - 1) % TE_STAGES, i - 1);
+                ++i;
+                first = false;
+                if (last) break;
+                cr = nr;
+                cz = nz;
+            }
+        }
+        int b;
+        acquire(b);
+        if (lane == 0) {
+            TileInfo inf{};
+            inf.flags = 8;  // done
+            *INFO_of(b) = inf;
+            mbar_arrive(&full[b]);
+        }
+        return;
+    }
+
+    // =============================== consumer warps ===============================
+    constexpr int S = 32 / G;
+    const int slot = lane / G;
+    const int gl = lane - slot * G;
+    bool colok[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) colok[v] = (gl * VEC + v * G * VEC) < n;
+    const char* Bl = opaque_ptr(static_cast<const char*>(P.B) + (size_t)gl * VEC * sizeof(T));
+    T* Cl = static_cast<T*>(P.C) + gl * VEC;
+    const unsigned ldb_bytes = P.ldb_bytes;
+
+    auto gather = [&](unsigned (&o)[NV][VEC], int c, bool ok) {
+        const char* bp = Bl + (size_t)(unsigned)c * ldb_bytes;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) ldg_pred<VEC>(o[v], bp + (size_t)v * G * VEC * sizeof(T), ok && colok[v]);
+    };
+    auto gather_full = [&](unsigned (&o)[NV][VEC], int c) {  // all columns valid when colok_all
+        const char* bp = Bl + (size_t)(unsigned)c * ldb_bytes;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            if (colok[v]) ldg_nc<VEC>(o[v], bp + (size_t)v * G * VEC * sizeof(T));
+        }
+    };
+    auto store_row = [&](long long row, const Acc<T, SR, VEC, NV>& acc, bool ok) {
+        T* crow = Cl + row * P.ldc;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            if (ok && colok[v]) {
+                unsigned o[VEC];
+#pragma unroll
+                for (int x = 0; x < VEC; ++x) o[x] = to_bits<T>(acc.v[v][x]);
+                st_vec<VEC>(crow + v * G * VEC, o);
+            }
+        }
+    };
+
+    if (MODE == MODE_MERGE && threadIdx.x == 0) { Crow[TE_CWARPS] = -1; Cflag[TE_CWARPS] = 0; }
+
+    for (int i = 0;; ++i) {
+        const int b = i % TE_STAGES;
+        mbar_wait(&full[b], (i / TE_STAGES) & 1);
+        const TileInfo inf = *INFO_of(b);
+        if (inf.flags & 8) break;
+        const int* E = E_of(b);
+        const int* COL = COL_of(b);
+        const T* VAL = VAL_of(b);
+        const bool staged = inf.flags & 4;
+
+        if (MODE == MODE_ROWSPLIT) {
+            // ---------------- Algorithm I: rows of the tile, one row per G-lane group ----------------
+            const int rows = inf.re - inf.rs;
+            const int NG = TE_CWARPS * S;
+            const int gid = warp * S + slot;
+            const int rounds = (rows + NG - 1) / NG;
+            for (int t = 0; t < rounds; ++t) {
+                const int lr = t * NG + gid;
+                const bool active = lr < rows;
+                const int s = active ? E[inf.rs + lr - inf.ebase] : 0;
+                const int e = active ? E[inf.rs + lr + 1 - inf.ebase] : 0;
+                const int len = e - s;
+                const int maxlen = __reduce_max_sync(FULL, len);
+                Acc<T, SR, VEC, NV> acc;
+                acc.reset();
+                if (staged) {
+                    const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(s - inf.zbase);
+                    const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(s - inf.zbase);
+                    for (int p0 = 0; p0 < maxlen; p0 += U) {
+                        const int rem = len - p0;
+                        unsigned bv[U][NV][VEC];
+                        unsigned cu[U], av[U];
+                        const bool full_b = rem >= U;
+                        if (__all_sync(FULL, full_b && ((cs & 15u) == 0))) {  // full, 16B-aligned: LDS.128
+#pragma unroll
+                            for (int u = 0; u < U; u += 4) {
+                                const uint4 c4 = lds_u128(cs + 4u * (p0 + u));
+                                const uint4 a4 = lds_u128(vs + 4u * (p0 + u));
+                                cu[u] = c4.x; cu[u + 1] = c4.y; cu[u + 2] = c4.z; cu[u + 3] = c4.w;
+                                av[u] = a4.x; av[u + 1] = a4.y; av[u + 2] = a4.z; av[u + 3] = a4.w;
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+#pragma unroll
+                            for (int u = 0; u < U; ++u) acc.mac(from_bits<T>(av[u]), bv[u]);
+                            continue;
+                        }
+                        if (__all_sync(FULL, full_b)) {  // full batch for every group of the warp
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                cu[u] = lds_u32(cs + 4u * (p0 + u));
+                                av[u] = lds_u32(vs + 4u * (p0 + u));
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+#pragma unroll
+                            for (int u = 0; u < U; ++u) acc.mac(from_bits<T>(av[u]), bv[u]);
+                            continue;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            cu[u] = lds_pred(cs + 4u * (p0 + u), u < rem);
+                            av[u] = lds_pred(vs + 4u * (p0 + u), u < rem);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) gather(bv[u], (int)cu[u], u < rem);
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (u < rem) acc.mac(from_bits<T>(av[u]), bv[u]);
+                    }
+                } else {  // tile too large for the staged slice (long rows): stream A from global
+                    const int* cg = P.col + s;
+                    const unsigned* vg = static_cast<const unsigned*>(P.val) + s;
+                    for (int p0 = 0; p0 < maxlen; p0 += U) {
+                        const int rem = len - p0;
+                        unsigned bv[U][NV][VEC];
+                        unsigned cu[U], av[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            cu[u] = ldg_stream_pred(cg + p0 + u, u < rem);
+                            av[u] = ldg_stream_pred(vg + p0 + u, u < rem);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) gather(bv[u], (int)cu[u], u < rem);
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (u < rem) acc.mac(from_bits<T>(av[u]), bv[u]);
+                    }
+                }
+                store_row(inf.rs + lr, acc, active);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);
+        } else {
+            // ---------------- Algorithm II: merge-path items, one worker per warp ----------------
+            const int rs = inf.rs, zs = inf.zs, re = inf.re, ze = inf.ze;
+            const int L = (re - rs) + (ze - zs);
+            const int per = (L + TE_CWARPS - 1) / TE_CWARPS;
+            const int* Eb = E + 1 - inf.ebase;  // Eb[x] = ro[x+1] (row end of row x)
+            auto search = [&](int d) -> int {
+                const int D = rs + zs + d;
+                int lo = max(rs, D - ze), hi = min(D - zs, re);
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (Eb[mid] <= D - mid - 1) lo = mid + 1; else hi = mid;
+                }
+                return lo;
+            };
+            if (inf.flags & 1) {  // first sub-tile of a range: no carry-in
+                if (threadIdx.x == 0) { Crow[TE_CWARPS] = -1; Cflag[TE_CWARPS] = 0; }
+                named_bar_sync(1, TE_CONSUMERS);
+            }
+            const int d0 = min(warp * per, L), d1 = min((warp + 1) * per, L);
+            const int ia = search(d0), ja = rs + zs + d0 - ia;
+            const int ib = search(d1), jb = rs + zs + d1 - ib;
+
+            Acc<T, SR, VEC, NV> acc;
+            bool dirty = false;
+            if (warp == 0 && Cflag[TE_CWARPS]) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int x = 0; x < VEC; ++x) {
+                        const int cc = gl * VEC + v * G * VEC + x;
+                        acc.v[v][x] = (cc < n) ? Cw[TE_CWARPS * n + cc] : R::id();
+                    }
+                dirty = true;
+            } else {
+                acc.reset();
+            }
+            int r = ia, q = ja;
+            int e = (r < m) ? Eb[r] : 0x7fffffff;
+            auto flush = [&]() {
+                store_row(r, acc, true);
+                acc.reset();
+                dirty = false;
+                ++r;
+                e = (r < m) ? Eb[r] : 0x7fffffff;
+            };
+            while (q < jb) {
+                const int cnt = min(U, jb - q);
+                unsigned bv[U][NV][VEC];
+                T av[U];
+                const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(q - inf.zbase);
+                const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(q - inf.zbase);
+                unsigned cu[U], au[U];
+                if (cnt == U && q + U <= e) {  // full batch inside the current row: no row end to check
+                    if ((cs & 15u) == 0) {
+#pragma unroll
+                        for (int u = 0; u < U; u += 4) {
+                            const uint4 c4 = lds_u128(cs + 4u * u);
+                            const uint4 a4 = lds_u128(vs + 4u * u);
+                            cu[u] = c4.x; cu[u + 1] = c4.y; cu[u + 2] = c4.z; cu[u + 3] = c4.w;
+                            au[u] = a4.x; au[u + 1] = a4.y; au[u + 2] = a4.z; au[u + 3] = a4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            cu[u] = lds_u32(cs + 4u * u);
+                            au[u] = lds_u32(vs + 4u * u);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) acc.mac(from_bits<T>(au[u]), bv[u]);
+                    dirty = true;
+                    q += U;
+                    continue;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    cu[u] = lds_pred(cs + 4u * u, u < cnt);
+                    au[u] = lds_pred(vs + 4u * u, u < cnt);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    av[u] = from_bits<T>(au[u]);
+                    gather(bv[u], (int)cu[u], u < cnt);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (u < cnt) {
+                        while (e <= q + u) flush();  // rows ending before nonzero q+u (rows first on ties)
+                        acc.mac(av[u], bv[u]);
+                        dirty = true;
+                    }
+                }
+                q += cnt;
+            }
+            while (r < ib) flush();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);  // done reading this buffer
+
+            // ---- worker carry -> shared slot; in-CTA resolution by warp 0 (ascending worker order)
+            if (lane == 0) { Crow[warp] = (int)ib; Cflag[warp] = dirty ? 1 : 0; }
+            if (dirty) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int x = 0; x < VEC; ++x) {
+                        const int cc = gl * VEC + v * G * VEC + x;
+                        if (colok[v]) Cw[warp * n + cc] = acc.v[v][x];
+                    }
+            }
+            named_bar_sync(1, TE_CONSUMERS);
+            if (warp == 0) {
+                int w = 0;
+                while (w < TE_CWARPS) {
+                    const int row = Crow[w];
+                    bool any = false;
+                    T sacc[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) sacc[t] = R::id();
+                    int w2 = w;
+                    while (w2 < TE_CWARPS && Crow[w2] == row) {
+                        if (Cflag[w2]) {
+                            any = true;
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const int cc = lane + 32 * t;
+                                if (cc < n) sacc[t] = R::add(sacc[t], Cw[w2 * n + cc]);
+                            }
+                        }
+                        ++w2;
+                    }
+                    if (row == (int)re) {  // the sub-tile's open row: carry it forward
+                        __syncwarp();
+                        if (lane == 0) { Crow[TE_CWARPS] = row; Cflag[TE_CWARPS] = any ? 1 : 0; }
+                        if (any) {
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const int cc = lane + 32 * t;
+                                if (cc < n) Cw[TE_CWARPS * n + cc] = sacc[t];
+                            }
+                        }
+                    } else if (any && row < m) {  // its owner already wrote C[row] in this sub-tile
+                        T* crow = static_cast<T*>(P.C) + (long long)row * P.ldc;
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int cc = lane + 32 * t;
+                            if (cc < n) crow[cc] = R::add(crow[cc], sacc[t]);
+                        }
+                    }
+                    w = w2;
+                }
+                __syncwarp();
+                if (inf.flags & 2) {  // last sub-tile of the range: CTA carry-out (Alg. 1 line 22)
+                    const int row = (re < m) ? (int)re : -1;
+                    const bool any = (row >= 0) && Cflag[TE_CWARPS] && Crow[TE_CWARPS] == row;
+                    if (lane == 0) { P.carry_row[inf.range] = row; P.carry_flag[inf.range] = any ? 1 : 0; }
+                    if (any) {
+                        T* cv = static_cast<T*>(P.carry_val) + (long long)inf.range * n;
+                        for (int cc = lane; cc < n; cc += 32) cv[cc] = Cw[TE_CWARPS * n + cc];
+                    }
+                }
+            }
+            named_bar_sync(1, TE_CONSUMERS);
+        }
+    }
+}
+
+}  // namespace spmm

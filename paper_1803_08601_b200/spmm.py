@@ -63,11 +63,13 @@ class SpmmError(RuntimeError):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load the in-tree libspmm.so (built by paper_1803_08601_b200.build / __graft_entry__.build())."""
+def load(path: str | None = None):
+    """Load the in-tree libspmm.so (built by paper_1803_08601_b200.build / __graft_entry__.build()).
+    SPMM_LIB=<path> selects an alternative in-tree build (tuning experiments only)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("SPMM_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"libspmm.so not found at {path}: run `python -m paper_1803_08601_b200.build` "
                            "(the CUDA path has no fallback)")
@@ -261,8 +263,11 @@ class CsrSpmm:
         return C
 
     def set_timing_events(self, events):
-        """events: list of torch.cuda.Event(enable_timing=True); see spmm_csr_set_timing_events."""
+        """events: list of torch.cuda.Event(enable_timing=True); see spmm_csr_set_timing_events.
+        torch creates the underlying cudaEvent_t lazily: record each event once before passing it."""
         self._events = list(events)  # keep alive
+        if any(e.cuda_event == 0 for e in self._events):
+            raise ValueError("torch.cuda.Event not created yet: call .record() once first")
         _check(spmm_csr_set_timing_events(self._h, [e.cuda_event for e in self._events]), self._h)
 
     def close(self):
