@@ -74,7 +74,7 @@ typedef struct {
                                 nonzeros) (default) or the paper's 1-D nonzero split
                                 (PAPER.md:80, :89).                                                  */
     int32_t items_per_cta;   /* merge-path items (rows + nonzeros) per CTA; 0 = default (2048).
-                                Must be a multiple of 256 in [256, 8192].                           */
+                                Must be a multiple of 256 in [256, 4096].                           */
     int32_t reserved[5];     /* must be zero */
 } spmm_plan_opts;
 

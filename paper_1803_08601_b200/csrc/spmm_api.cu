@@ -43,14 +43,23 @@ struct spmm_csr_s {
 
 namespace {
 
-constexpr int kDefaultItems = 2048;
 constexpr int kNumSMs = 148;
 #ifndef RS_U
-#define RS_U 8
+#define RS_U 16
 #endif
 #ifndef MG_U
 #define MG_U 16
 #endif
+#ifndef RS_STAGES
+#define RS_STAGES 3
+#endif
+#ifndef MG_SMEM_BUDGET
+#define MG_SMEM_BUDGET 75000  // bytes of staged CSR tiles per merge CTA (stages = budget / tile bytes)
+#endif
+#ifndef MG_ITEMS
+#define MG_ITEMS 2048
+#endif
+constexpr int kDefaultItems = MG_ITEMS;
 constexpr int kRowsplitU = RS_U;
 constexpr int kMergeU = MG_U;
 
@@ -147,7 +156,7 @@ int num_sms() {
 template <typename T, int SR, int MODE, int V, int G, int NV, int U>
 cudaError_t launch_tile(const TileParams& P, cudaStream_t st) {
     auto kfn = k_tile<T, SR, MODE, V, G, NV, U>;
-    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n);
+    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages);
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -166,6 +175,7 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
     P.rows_per_tile = h->rows_per_tile;
     P.capr = h->rows_per_tile + 8;
     P.capz = h->capz;
+    P.stages = RS_STAGES;
     mark(h, 0, st);
     cudaError_t e;
 #define RS_CASE(V, G_, NV_) \
@@ -212,6 +222,7 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     P.carry_val = carry_val;
     P.capr = items + 8;
     P.capz = items + 8;
+    P.stages = std::max(2, std::min(TE_MAX_STAGES, (int)(MG_SMEM_BUDGET / te_buf_bytes(P.capr, P.capz, (int)sizeof(T)))));
 #define MG_CASE(V, NV_) \
     case (V)*10 + (NV_): e = launch_tile<T, SR, MODE_MERGE, V, 32, NV_, kMergeU>(P, st); break;
     switch (cfg.vec * 10 + cfg.NV) {
@@ -358,8 +369,8 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     if (o.partition != SPMM_PARTITION_MERGE_PATH && o.partition != SPMM_PARTITION_NONZERO_SPLIT)
         return fail(h, SPMM_ERR_INVALID_ARG, "bad partition");
     int items = o.items_per_cta ? o.items_per_cta : kDefaultItems;
-    if (items < 256 || items > 8192 || items % 256 != 0)
-        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 256 in [256, 8192]");
+    if (items < 256 || items > 4096 || items % 256 != 0)
+        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 256 in [256, 4096]");
     o.items_per_cta = items;
     h->threshold = threshold > 0 ? threshold : 9.35;
     h->n = n;

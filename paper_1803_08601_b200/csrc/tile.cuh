@@ -27,16 +27,16 @@
 
 namespace spmm {
 
-constexpr int TE_CWARPS = 8;                    // consumer warps
+#ifndef TE_CWARPS_DEF
+#define TE_CWARPS_DEF 8
+#endif
+constexpr int TE_CWARPS = TE_CWARPS_DEF;        // consumer warps
 constexpr int TE_THREADS = 32 * (TE_CWARPS + 1);  // + 1 producer warp
 constexpr int TE_CONSUMERS = 32 * TE_CWARPS;
-#ifndef TE_STAGES_DEF
-#define TE_STAGES_DEF 3
-#endif
 #ifndef TE_MINB
 #define TE_MINB 2  // CTAs per SM the register allocation targets (__launch_bounds__)
 #endif
-constexpr int TE_STAGES = TE_STAGES_DEF;        // shared-memory pipeline depth (tiles in flight)
+constexpr int TE_MAX_STAGES = 8;                // shared-memory pipeline depth limit (tiles in flight)
 enum : int { MODE_ROWSPLIT = 0, MODE_MERGE = 1 };
 
 struct TileParams {
@@ -57,6 +57,7 @@ struct TileParams {
     void* carry_val;
     int capr, capz;     // elements per buffer: row offsets / (col, val)
     unsigned pf_bytes;  // bytes of each B row to prefetch into L2 ahead of the consumers (0 = off)
+    int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
 };
 
 // tile descriptor written by the producer next to the staged data
@@ -70,9 +71,10 @@ struct TileInfo {
 __host__ __device__ inline size_t te_buf_bytes(int capr, int capz, int elem) {
     return (size_t)capr * 4 + (size_t)capz * 4 + (size_t)capz * elem + 64;
 }
-__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n) {
-    return TE_STAGES * te_buf_bytes(capr, capz, elem) + 64 /*barriers*/ +
-           (size_t)(TE_CWARPS + 1) * n * elem + (size_t)(TE_CWARPS + 1) * 8 + 64;
+__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n, int stages) {
+    return stages * te_buf_bytes(capr, capz, elem) + 16 * TE_MAX_STAGES /*barriers*/ +
+           (size_t)(TE_CWARPS + 1) * n * elem + (size_t)(TE_CWARPS + 1) * 8 + 64 +
+           (size_t)stages * TE_CWARPS * n * elem + (size_t)stages * TE_CWARPS * 8 + stages * 4 + 64;
 }
 
 // stage global src[begin, end) (4-byte elements, arr_len elements in the array) at dst; returns the
@@ -124,6 +126,12 @@ template <typename T, int SR, int VEC, int NV> struct Acc {
 #pragma unroll
             for (int x = 0; x < VEC; ++x) v[a][x] = Ring<T, SR>::id();
     }
+    __device__ __forceinline__ void fold(const Acc& o) {  // this (+)= o
+#pragma unroll
+        for (int a = 0; a < NV; ++a)
+#pragma unroll
+            for (int x = 0; x < VEC; ++x) v[a][x] = Ring<T, SR>::add(v[a][x], o.v[a][x]);
+    }
     __device__ __forceinline__ void mac(T a, const unsigned (&b)[NV][VEC]) {
         if constexpr (std::is_same<T, float>::value && SR == SR_PLUS_TIMES && VEC % 2 == 0) {
             const float2 aa = make_float2(a, a);
@@ -158,17 +166,23 @@ k_tile(const TileParams P) {
     auto INFO_of = [&](int b) {
         return reinterpret_cast<TileInfo*>(smem + b * bufb + (size_t)capr * 4 + (size_t)capz * (4 + sizeof(T)));
     };
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + TE_STAGES * bufb);
-    uint64_t* empty = full + TE_STAGES;
-    T* Cw = reinterpret_cast<T*>(smem + TE_STAGES * bufb + 64);                 // [W+1][n] worker carries
+    const int NS = P.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * bufb);
+    uint64_t* empty = full + TE_MAX_STAGES;
+    T* Cw = reinterpret_cast<T*>(smem + NS * bufb + 16 * TE_MAX_STAGES);                 // [W+1][n] worker carries
     int* Crow = reinterpret_cast<int*>(Cw + (size_t)(TE_CWARPS + 1) * n);  // [W+1]
     int* Cflag = Crow + (TE_CWARPS + 1);                                 // [W+1]
+    // per-stage worker carry slots for the barrier-free resolution of single-tile ranges
+    T* CwS = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(Cflag + (TE_CWARPS + 1)) + 64);  // [S][W][n]
+    int* CrowS = reinterpret_cast<int*>(CwS + (size_t)NS * TE_CWARPS * n);                   // [S][W]
+    int* CflagS = CrowS + NS * TE_CWARPS;                                                     // [S][W]
+    int* Ccnt = CflagS + NS * TE_CWARPS;                                                      // [S]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TE_STAGES; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], TE_CWARPS);
         }
@@ -181,15 +195,17 @@ k_tile(const TileParams P) {
         const uint64_t pol = policy_evict_first();
         int i = 0;
         auto acquire = [&](int& b) {
-            b = i % TE_STAGES;
-            if (i >= TE_STAGES) mbar_wait(&empty[b], ((i / TE_STAGES) - 1) & 1);
+            b = i % NS;
+            if (i >= NS) {
+                while (!mbar_try_wait(&empty[b], ((i / NS) - 1) & 1)) __nanosleep(64);
+            }
         };
         // L2 prefetch of the B rows a staged tile will gather, when the tile's columns are clustered
         // (banded / mesh-like matrices): one TMA bulk prefetch (cp.async.bulk.prefetch.L2) of the
         // tile's B row span, issued once the tile's column indices have landed in shared memory, so
         // the consumers' first-touch gathers hit L2 instead of paying a DRAM round trip.
         auto prefetch_tile_b = [&](int pb, int ti) {
-            mbar_wait(&full[pb], (ti / TE_STAGES) & 1);
+            mbar_wait(&full[pb], (ti / NS) & 1);
             const TileInfo pi = *INFO_of(pb);
             if (!(pi.flags & 4)) return;
             const int cnt = pi.ze - pi.zs;
@@ -266,7 +282,7 @@ k_tile(const TileParams P) {
                     mbar_arrive_expect_tx(&full[b], tx);
                 }
                 __syncwarp();
-                if (P.pf_bytes && i >= 1) prefetch_tile_b((i - 1) % TE_STAGES, i - 1);
+                if (MODE == MODE_ROWSPLIT && P.pf_bytes && i >= 1) prefetch_tile_b((i - 1) % NS, i - 1);
                 ++i;
                 first = false;
                 if (last) break;
@@ -287,26 +303,30 @@ k_tile(const TileParams P) {
 
     // =============================== consumer warps ===============================
     constexpr int S = 32 / G;
+    constexpr int NA = (MODE == MODE_MERGE) ? ((VEC * NV <= 2) ? 4 : 2) : 2;
     const int slot = lane / G;
     const int gl = lane - slot * G;
     bool colok[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) colok[v] = (gl * VEC + v * G * VEC) < n;
-    const char* Bl = opaque_ptr(static_cast<const char*>(P.B) + (size_t)gl * VEC * sizeof(T));
+    // per-lane B base of each column block; lanes past n read column 0 of the same row instead
+    // (valid memory, never stored), so the gathers need no column predicate or branch
+    const char* Blv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+        Blv[v] = opaque_ptr(static_cast<const char*>(P.B) +
+                            (colok[v] ? (size_t)(gl * VEC + v * G * VEC) * sizeof(T) : (size_t)0));
+    const char* Bl = Blv[0];
     T* Cl = static_cast<T*>(P.C) + gl * VEC;
     const unsigned ldb_bytes = P.ldb_bytes;
 
     auto gather = [&](unsigned (&o)[NV][VEC], int c, bool ok) {
-        const char* bp = Bl + (size_t)(unsigned)c * ldb_bytes;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) ldg_pred<VEC>(o[v], bp + (size_t)v * G * VEC * sizeof(T), ok && colok[v]);
+        for (int v = 0; v < NV; ++v) ldg_pred<VEC>(o[v], Blv[v] + (size_t)(unsigned)c * ldb_bytes, ok);
     };
-    auto gather_full = [&](unsigned (&o)[NV][VEC], int c) {  // all columns valid when colok_all
-        const char* bp = Bl + (size_t)(unsigned)c * ldb_bytes;
+    auto gather_full = [&](unsigned (&o)[NV][VEC], int c) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            if (colok[v]) ldg_nc<VEC>(o[v], bp + (size_t)v * G * VEC * sizeof(T));
-        }
+        for (int v = 0; v < NV; ++v) ldg_nc<VEC>(o[v], Blv[v] + (size_t)(unsigned)c * ldb_bytes);
     };
     auto store_row = [&](long long row, const Acc<T, SR, VEC, NV>& acc, bool ok) {
         T* crow = Cl + row * P.ldc;
@@ -321,11 +341,16 @@ k_tile(const TileParams P) {
         }
     };
 
-    if (MODE == MODE_MERGE && threadIdx.x == 0) { Crow[TE_CWARPS] = -1; Cflag[TE_CWARPS] = 0; }
+    if (MODE == MODE_MERGE && threadIdx.x == 0) {
+        Crow[TE_CWARPS] = -1;
+        Cflag[TE_CWARPS] = 0;
+        for (int s = 0; s < NS; ++s) Ccnt[s] = 0;
+    }
+    if (MODE == MODE_MERGE) named_bar_sync(1, TE_CONSUMERS);
 
     for (int i = 0;; ++i) {
-        const int b = i % TE_STAGES;
-        mbar_wait(&full[b], (i / TE_STAGES) & 1);
+        const int b = i % NS;
+        mbar_wait(&full[b], (i / NS) & 1);
         const TileInfo inf = *INFO_of(b);
         if (inf.flags & 8) break;
         const int* E = E_of(b);
@@ -346,8 +371,9 @@ k_tile(const TileParams P) {
                 const int e = active ? E[inf.rs + lr + 1 - inf.ebase] : 0;
                 const int len = e - s;
                 const int maxlen = __reduce_max_sync(FULL, len);
-                Acc<T, SR, VEC, NV> acc;
-                acc.reset();
+                Acc<T, SR, VEC, NV> accs[NA];  // NA interleaved partial sums: short FMA dependency chains
+#pragma unroll
+                for (int k = 0; k < NA; ++k) accs[k].reset();
                 if (staged) {
                     const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(s - inf.zbase);
                     const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(s - inf.zbase);
@@ -356,6 +382,21 @@ k_tile(const TileParams P) {
                         unsigned bv[U][NV][VEC];
                         unsigned cu[U], av[U];
                         const bool full_b = rem >= U;
+#ifdef RS_SHFL
+                        if (G >= 2 * U && __all_sync(FULL, full_b)) {  // one LDS per lane + shuffles
+                            const unsigned x = lds_u32(gl < U ? cs + 4u * (p0 + gl) : vs + 4u * (p0 + gl - U));
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                cu[u] = __shfl_sync(FULL, x, u, G);
+                                av[u] = __shfl_sync(FULL, x, U + u, G);
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+#pragma unroll
+                            for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
+                            continue;
+                        }
+#endif
                         if (__all_sync(FULL, full_b && ((cs & 15u) == 0))) {  // full, 16B-aligned: LDS.128
 #pragma unroll
                             for (int u = 0; u < U; u += 4) {
@@ -367,7 +408,7 @@ k_tile(const TileParams P) {
 #pragma unroll
                             for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
 #pragma unroll
-                            for (int u = 0; u < U; ++u) acc.mac(from_bits<T>(av[u]), bv[u]);
+                            for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                             continue;
                         }
                         if (__all_sync(FULL, full_b)) {  // full batch for every group of the warp
@@ -379,7 +420,7 @@ k_tile(const TileParams P) {
 #pragma unroll
                             for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
 #pragma unroll
-                            for (int u = 0; u < U; ++u) acc.mac(from_bits<T>(av[u]), bv[u]);
+                            for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                             continue;
                         }
 #pragma unroll
@@ -391,7 +432,7 @@ k_tile(const TileParams P) {
                         for (int u = 0; u < U; ++u) gather(bv[u], (int)cu[u], u < rem);
 #pragma unroll
                         for (int u = 0; u < U; ++u)
-                            if (u < rem) acc.mac(from_bits<T>(av[u]), bv[u]);
+                            if (u < rem) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                     }
                 } else {  // tile too large for the staged slice (long rows): stream A from global
                     const int* cg = P.col + s;
@@ -409,10 +450,12 @@ k_tile(const TileParams P) {
                         for (int u = 0; u < U; ++u) gather(bv[u], (int)cu[u], u < rem);
 #pragma unroll
                         for (int u = 0; u < U; ++u)
-                            if (u < rem) acc.mac(from_bits<T>(av[u]), bv[u]);
+                            if (u < rem) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                     }
                 }
-                store_row(inf.rs + lr, acc, active);
+#pragma unroll
+                for (int k = 1; k < NA; ++k) accs[0].fold(accs[k]);
+                store_row(inf.rs + lr, accs[0], active);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[b]);
@@ -431,17 +474,16 @@ k_tile(const TileParams P) {
                 }
                 return lo;
             };
-            if (inf.flags & 1) {  // first sub-tile of a range: no carry-in
-                if (threadIdx.x == 0) { Crow[TE_CWARPS] = -1; Cflag[TE_CWARPS] = 0; }
-                named_bar_sync(1, TE_CONSUMERS);
-            }
             const int d0 = min(warp * per, L), d1 = min((warp + 1) * per, L);
             const int ia = search(d0), ja = rs + zs + d0 - ia;
             const int ib = search(d1), jb = rs + zs + d1 - ib;
 
-            Acc<T, SR, VEC, NV> acc;
+            Acc<T, SR, VEC, NV> accs[NA];  // NA interleaved partial sums: short FMA dependency chains
+#pragma unroll
+            for (int k = 1; k < NA; ++k) accs[k].reset();
+            Acc<T, SR, VEC, NV>& acc = accs[0];
             bool dirty = false;
-            if (warp == 0 && Cflag[TE_CWARPS]) {
+            if (warp == 0 && !(inf.flags & 1) && Cflag[TE_CWARPS]) {  // carry-in from the previous sub-tile
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -455,19 +497,38 @@ k_tile(const TileParams P) {
             }
             int r = ia, q = ja;
             int e = (r < m) ? Eb[r] : 0x7fffffff;
+            auto collapse = [&]() {
+#pragma unroll
+                for (int k = 1; k < NA; ++k) {
+                    accs[0].fold(accs[k]);
+                    accs[k].reset();
+                }
+            };
             auto flush = [&]() {
+                collapse();
                 store_row(r, acc, true);
                 acc.reset();
                 dirty = false;
                 ++r;
                 e = (r < m) ? Eb[r] : 0x7fffffff;
             };
+#ifndef MG_PF
+#define MG_PF 0
+#endif
             while (q < jb) {
                 const int cnt = min(U, jb - q);
                 unsigned bv[U][NV][VEC];
                 T av[U];
                 const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(q - inf.zbase);
                 const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(q - inf.zbase);
+                if (MG_PF > 0) {
+                    // software prefetch into L2 of the B rows gathered MG_PF nonzeros ahead: turns the
+                    // DRAM misses of the next batch into L2 hits without holding registers
+                    const int pq = q + MG_PF;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (pq + u < jb) prefetch_l2(Bl + (size_t)lds_u32(cs + 4u * (MG_PF + u)) * ldb_bytes);
+                }
                 unsigned cu[U], au[U];
                 if (cnt == U && q + U <= e) {  // full batch inside the current row: no row end to check
                     if ((cs & 15u) == 0) {
@@ -488,7 +549,7 @@ k_tile(const TileParams P) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) acc.mac(from_bits<T>(au[u]), bv[u]);
+                    for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(au[u]), bv[u]);
                     dirty = true;
                     q += U;
                     continue;
@@ -507,78 +568,130 @@ k_tile(const TileParams P) {
                 for (int u = 0; u < U; ++u) {
                     if (u < cnt) {
                         while (e <= q + u) flush();  // rows ending before nonzero q+u (rows first on ties)
-                        acc.mac(av[u], bv[u]);
+                        accs[u % NA].mac(av[u], bv[u]);
                         dirty = true;
                     }
                 }
                 q += cnt;
             }
             while (r < ib) flush();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[b]);  // done reading this buffer
+            collapse();
 
-            // ---- worker carry -> shared slot; in-CTA resolution by warp 0 (ascending worker order)
-            if (lane == 0) { Crow[warp] = (int)ib; Cflag[warp] = dirty ? 1 : 0; }
-            if (dirty) {
+            // ---- carry resolution (Alg. 1 line 22): sums worker partials of the same row in ascending
+            // worker order; rows whose end item lies in this sub-tile were already written by their
+            // owner and get the sum added (RMW); the sub-tile's open row `re` is returned in `open`.
+            auto resolve = [&](const T* slots, const int* srow, const int* sflag, T (&open)[4], bool& open_any) {
+                open_any = false;
 #pragma unroll
-                for (int v = 0; v < NV; ++v)
-#pragma unroll
-                    for (int x = 0; x < VEC; ++x) {
-                        const int cc = gl * VEC + v * G * VEC + x;
-                        if (colok[v]) Cw[warp * n + cc] = acc.v[v][x];
-                    }
-            }
-            named_bar_sync(1, TE_CONSUMERS);
-            if (warp == 0) {
+                for (int t2 = 0; t2 < 4; ++t2) open[t2] = R::id();
                 int w = 0;
                 while (w < TE_CWARPS) {
-                    const int row = Crow[w];
+                    const int row = srow[w];
                     bool any = false;
                     T sacc[4];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) sacc[t] = R::id();
+                    for (int t2 = 0; t2 < 4; ++t2) sacc[t2] = R::id();
                     int w2 = w;
-                    while (w2 < TE_CWARPS && Crow[w2] == row) {
-                        if (Cflag[w2]) {
+                    while (w2 < TE_CWARPS && srow[w2] == row) {
+                        if (sflag[w2]) {
                             any = true;
 #pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                const int cc = lane + 32 * t;
-                                if (cc < n) sacc[t] = R::add(sacc[t], Cw[w2 * n + cc]);
+                            for (int t2 = 0; t2 < 4; ++t2) {
+                                const int cc = lane + 32 * t2;
+                                if (cc < n) sacc[t2] = R::add(sacc[t2], slots[w2 * n + cc]);
                             }
                         }
                         ++w2;
                     }
-                    if (row == (int)re) {  // the sub-tile's open row: carry it forward
-                        __syncwarp();
-                        if (lane == 0) { Crow[TE_CWARPS] = row; Cflag[TE_CWARPS] = any ? 1 : 0; }
-                        if (any) {
+                    if (row == re) {
+                        open_any = any;
 #pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                const int cc = lane + 32 * t;
-                                if (cc < n) Cw[TE_CWARPS * n + cc] = sacc[t];
-                            }
-                        }
-                    } else if (any && row < m) {  // its owner already wrote C[row] in this sub-tile
+                        for (int t2 = 0; t2 < 4; ++t2) open[t2] = sacc[t2];
+                    } else if (any && row < m) {
                         T* crow = static_cast<T*>(P.C) + (long long)row * P.ldc;
 #pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const int cc = lane + 32 * t;
-                            if (cc < n) crow[cc] = R::add(crow[cc], sacc[t]);
+                        for (int t2 = 0; t2 < 4; ++t2) {
+                            const int cc = lane + 32 * t2;
+                            if (cc < n) crow[cc] = R::add(__ldcg(crow + cc), sacc[t2]);
                         }
                     }
                     w = w2;
                 }
-                __syncwarp();
-                if (inf.flags & 2) {  // last sub-tile of the range: CTA carry-out (Alg. 1 line 22)
-                    const int row = (re < m) ? (int)re : -1;
-                    const bool any = (row >= 0) && Cflag[TE_CWARPS] && Crow[TE_CWARPS] == row;
-                    if (lane == 0) { P.carry_row[inf.range] = row; P.carry_flag[inf.range] = any ? 1 : 0; }
-                    if (any) {
-                        T* cv = static_cast<T*>(P.carry_val) + (long long)inf.range * n;
-                        for (int cc = lane; cc < n; cc += 32) cv[cc] = Cw[TE_CWARPS * n + cc];
+            };
+            auto write_global_carry = [&](const T (&open)[4], bool open_any) {
+                const int row = (re < m) ? re : -1;
+                const bool any = (row >= 0) && open_any;
+                if (lane == 0) { P.carry_row[inf.range] = row; P.carry_flag[inf.range] = any ? 1 : 0; }
+                if (any) {
+                    T* cv = static_cast<T*>(P.carry_val) + (long long)inf.range * n;
+#pragma unroll
+                    for (int t2 = 0; t2 < 4; ++t2) {
+                        const int cc = lane + 32 * t2;
+                        if (cc < n) cv[cc] = open[t2];
                     }
                 }
+            };
+            auto publish = [&](T* slots, int* srow, int* sflag) {
+                if (lane == 0) { srow[warp] = ib; sflag[warp] = dirty ? 1 : 0; }
+                if (dirty) {
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+#pragma unroll
+                        for (int x = 0; x < VEC; ++x) {
+                            const int cc = gl * VEC + v * G * VEC + x;
+                            if (colok[v]) slots[warp * n + cc] = acc.v[v][x];
+                        }
+                }
+            };
+
+            if ((inf.flags & 3) == 3) {
+                // whole range in one tile (2-D merge path): barrier-free -- the last worker to finish
+                // resolves the carries, the others move straight on to their next tile
+                T* slots = CwS + (size_t)b * TE_CWARPS * n;
+                int* srow = CrowS + b * TE_CWARPS;
+                int* sflag = CflagS + b * TE_CWARPS;
+                publish(slots, srow, sflag);
+                __syncwarp();
+                int last = 0;
+                if (lane == 0) {
+                    __threadfence_block();
+                    last = (atomicAdd(&Ccnt[b], 1) == TE_CWARPS - 1) ? 1 : 0;
+                }
+                last = __shfl_sync(FULL, last, 0);
+                if (last) {
+                    __threadfence_block();
+                    T open[4];
+                    bool open_any;
+                    resolve(slots, srow, sflag, open, open_any);
+                    write_global_carry(open, open_any);
+                    __syncwarp();
+                    if (lane == 0) Ccnt[b] = 0;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[b]);  // buffer and slots of stage b are free
+                continue;
+            }
+
+            // range split over several sub-tiles (1-D nonzero split with many rows): synchronous
+            // resolution with a carry forwarded to the next sub-tile's first worker
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[b]);  // done reading this buffer
+            publish(Cw, Crow, Cflag);
+            named_bar_sync(1, TE_CONSUMERS);
+            if (warp == 0) {
+                T open[4];
+                bool open_any;
+                resolve(Cw, Crow, Cflag, open, open_any);
+                __syncwarp();
+                if (lane == 0) { Crow[TE_CWARPS] = re; Cflag[TE_CWARPS] = open_any ? 1 : 0; }
+                if (open_any) {
+#pragma unroll
+                    for (int t2 = 0; t2 < 4; ++t2) {
+                        const int cc = lane + 32 * t2;
+                        if (cc < n) Cw[TE_CWARPS * n + cc] = open[t2];
+                    }
+                }
+                if (inf.flags & 2) write_global_carry(open, open_any);
             }
             named_bar_sync(1, TE_CONSUMERS);
         }
