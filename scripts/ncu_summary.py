@@ -56,8 +56,31 @@ def stalls(rep, top=25):
     return tot_e, tot_w, items[:top]
 
 
+def stall_reasons(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, v = rows[0], rows[2]
+    res = [(h.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(x)) for h, x in zip(hdr, v)
+           if "pcsamp_warps_issue_stalled" in h and not h.endswith("not_issued") and x.replace(".", "").isdigit()]
+    tot = sum(x for _, x in res) or 1.0
+    return [(h, x / tot) for h, x in sorted(res, key=lambda t: -t[1])]
+
+
 if __name__ == "__main__":
     rep = sys.argv[1]
+    if "--json" in sys.argv:
+        import json
+        import os
+        r = raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"])
+        def val(k, scale):
+            v, u = r[k][0]
+            f = float(v)
+            return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+                        "msecond": 1e-3, "second": 1}.get(u, scale)
+        print(json.dumps({"report": os.path.basename(rep), "dram_read_bytes": val("dram__bytes_read.sum", 1),
+                          "dram_write_bytes": val("dram__bytes_write.sum", 1),
+                          "duration_s": val("gpu__time_duration.sum", 1)}))
+        sys.exit(0)
     for k in details(rep):
         print(f"{k[1]:<40} {k[3]:>16} {k[2]}")
     r = raw(rep, ["dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
@@ -65,6 +88,8 @@ if __name__ == "__main__":
                   "l1tex__t_sector_hit_rate.pct", "lts__t_bytes.sum", "l1tex__t_bytes.sum"])
     for k, v in r.items():
         print(f"{k:<55} {v}")
+    for h, f in stall_reasons(rep)[:8]:
+        print(f"stall {h:<30} {f * 100:5.1f}%")
     if "--stalls" in sys.argv:
         te, tw, items = stalls(rep)
         print(f"instructions executed {te}, stall samples {tw}")
