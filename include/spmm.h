@@ -11,8 +11,8 @@
  *   SPMM_ALGO_ROWSPLIT  row splitting, §4.1 (Fig. 3, Table 1)
  *   SPMM_ALGO_MERGE     merge-based, §4.2 Algorithm 1: PartitionSpmm (line 2),
  *                       per-CTA compute with carry-out (lines 3-23), FixCarryOut (line 24)
- *   SPMM_ALGO_AUTO      §5.4 heuristic: merge iff mean row length d = nnz/m < threshold
- *                       (default 9.35), plus (policy AUTO) a skew guard, see spmm_plan_opts.
+ *   SPMM_ALGO_AUTO      §5.4 heuristic: policy PAPER = merge iff mean row length d = nnz/m < threshold
+ *                       (default 9.35); policy AUTO = B200 refit, see spmm_plan_opts.
  *
  * Conventions (all entry points):
  *   - Every pointer named row_offsets / col_indices / values / B / C / workspace is a DEVICE pointer
@@ -67,9 +67,10 @@ typedef enum { SPMM_PARTITION_MERGE_PATH = 0, SPMM_PARTITION_NONZERO_SPLIT = 1 }
 /* Optional planner knobs (spmm_csr_plan_ex).  Zero-initialised = defaults. */
 typedef struct {
     int32_t policy;          /* spmm_policy.  PAPER: merge iff d < threshold.
-                                AUTO (default): PAPER rule, OR merge when the longest row exceeds
-                                the per-warp fair share nnz/(148*32) and is > 8x the mean
-                                (costs one O(m) device reduction + sync). */
+                                AUTO (default): B200 refit of §5.4 -- merge iff the row
+                                lengths are skewed (max row > 16 d and >= 1024) or there are too few
+                                rows to fill the row-split kernel (m < 2 x resident row groups);
+                                costs one O(m) device reduction + stream sync at plan time.  */
     int32_t partition;       /* spmm_partition for the merge kernel: 2-D merge path over (row ends,
                                 nonzeros) (default) or the paper's 1-D nonzero split
                                 (PAPER.md:80, :89).                                                  */

@@ -45,13 +45,22 @@ namespace {
 
 constexpr int kNumSMs = 148;
 #ifndef RS_U
-#define RS_U 16
+#define RS_U 8
 #endif
 #ifndef MG_U
 #define MG_U 16
 #endif
+#ifndef MG_FOLD
+#define MG_FOLD 0  // merge with lane-folded workers for n <= 16 (experimental; slower on B200 so far)
+#endif
 #ifndef RS_STAGES
 #define RS_STAGES 3
+#endif
+#ifndef RS_TILE_NNZ
+#define RS_TILE_NNZ 2048  // row split: target nonzeros per row tile
+#endif
+#ifndef RS_ZF
+#define RS_ZF 12  // row split: staged capacity = RS_ZF/10 x the tile's expected nonzeros
 #endif
 #ifndef MG_SMEM_BUDGET
 #define MG_SMEM_BUDGET 75000  // bytes of staged CSR tiles per merge CTA (stages = budget / tile bytes)
@@ -128,9 +137,20 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
     VecCfg c;
     c.vec = vec;
     if (folded) {
-        c.G = std::min(32, pow2ceil(lanes));
-        c.NV = (lanes + 31) / 32;
-    } else {  // one worker per warp: narrowest vector that covers n with 32 lanes
+        // row groups of G lanes; for 16..32 lanes split the row over half as many lanes with two
+        // column blocks each (n = 64: 8 lanes x 2 float4) -- more rows per warp, fewer broadcast loads
+        const int G0 = std::min(32, pow2ceil(lanes));
+        if (lanes <= 32 && G0 >= 16) {
+            c.G = G0 / 2;
+            c.NV = (lanes + c.G - 1) / c.G;
+        } else {
+            c.G = G0;
+            c.NV = (lanes + 31) / 32;
+        }
+    } else if (MG_FOLD && n <= 16) {  // merge, small n: lane-folded workers of G lanes (32/G per warp)
+        c.G = pow2ceil(lanes);
+        c.NV = 1;
+    } else {  // merge: one worker per warp, narrowest vector that covers n with 32 lanes
         const int want = n <= 32 ? 1 : (n <= 64 ? 2 : 4);
         if (want < vec) c.vec = want;
         const int l2 = (n + c.vec - 1) / c.vec;
@@ -156,7 +176,7 @@ int num_sms() {
 template <typename T, int SR, int MODE, int V, int G, int NV, int U>
 cudaError_t launch_tile(const TileParams& P, cudaStream_t st) {
     auto kfn = k_tile<T, SR, MODE, V, G, NV, U>;
-    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages);
+    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G));
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -181,10 +201,10 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
 #define RS_CASE(V, G_, NV_) \
     case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kRowsplitU>(P, st); break;
     switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
-        RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 16, 1) RS_CASE(4, 32, 1)
-        RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 16, 1) RS_CASE(2, 32, 1)
+        RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 8, 2) RS_CASE(4, 16, 2)
+        RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 8, 2) RS_CASE(2, 16, 2)
         RS_CASE(2, 32, 2)
-        RS_CASE(1, 1, 1) RS_CASE(1, 2, 1) RS_CASE(1, 4, 1) RS_CASE(1, 8, 1) RS_CASE(1, 16, 1) RS_CASE(1, 32, 1)
+        RS_CASE(1, 1, 1) RS_CASE(1, 2, 1) RS_CASE(1, 4, 1) RS_CASE(1, 8, 1) RS_CASE(1, 8, 2) RS_CASE(1, 16, 2)
         RS_CASE(1, 32, 2) RS_CASE(1, 32, 3) RS_CASE(1, 32, 4)
         default: return cudaErrorNotSupported;
     }
@@ -223,10 +243,15 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     P.capr = items + 8;
     P.capz = items + 8;
     P.stages = std::max(2, std::min(TE_MAX_STAGES, (int)(MG_SMEM_BUDGET / te_buf_bytes(P.capr, P.capz, (int)sizeof(T)))));
-#define MG_CASE(V, NV_) \
-    case (V)*10 + (NV_): e = launch_tile<T, SR, MODE_MERGE, V, 32, NV_, kMergeU>(P, st); break;
-    switch (cfg.vec * 10 + cfg.NV) {
-        MG_CASE(4, 1) MG_CASE(2, 1) MG_CASE(2, 2) MG_CASE(1, 1) MG_CASE(1, 2) MG_CASE(1, 3) MG_CASE(1, 4)
+#define MG_CASE(V, G_, NV_) \
+    case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_MERGE, V, G_, NV_, kMergeU>(P, st); break;
+    switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
+        MG_CASE(4, 32, 1) MG_CASE(2, 32, 1) MG_CASE(2, 32, 2) MG_CASE(1, 32, 1) MG_CASE(1, 32, 2) MG_CASE(1, 32, 3)
+        MG_CASE(1, 32, 4)
+#if MG_FOLD
+        MG_CASE(4, 1, 1) MG_CASE(4, 2, 1) MG_CASE(4, 4, 1) MG_CASE(2, 1, 1) MG_CASE(2, 2, 1) MG_CASE(2, 4, 1)
+        MG_CASE(2, 8, 1) MG_CASE(1, 1, 1) MG_CASE(1, 2, 1) MG_CASE(1, 4, 1) MG_CASE(1, 8, 1) MG_CASE(1, 16, 1)
+#endif
         default: return cudaErrorNotSupported;
     }
 #undef MG_CASE
@@ -381,11 +406,15 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     const double d = h->m > 0 ? (double)h->nnz / (double)h->m : 0.0;  // PAPER.md:267, mean row length
     spmm_algo pick = algo;
     if (algo == SPMM_ALGO_AUTO) {
-        // §5.4: "use merge-based on datasets whose mean row length is less than 9.35, and row split otherwise"
-        pick = (d < h->threshold) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
-        if (pick == SPMM_ALGO_ROWSPLIT && o.policy == SPMM_POLICY_AUTO && h->m > 0) {
-            // skew guard: a row longer than the per-warp fair share makes row split a
-            // straggler (Type 1 imbalance); merge path balances it.
+        if (o.policy == SPMM_POLICY_PAPER || h->m == 0) {
+            // §5.4: "use merge-based on datasets whose mean row length is less than 9.35, and row split
+            // otherwise"
+            pick = (d < h->threshold) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
+        } else {
+            // AUTO (B200 refit of §5.4, profiles/r01_config4_*): on this GPU the row-split
+            // kernel handles short rows well, so the row-length threshold is replaced by the two causes of
+            // Type 1 imbalance that merge path removes: a skewed row-length
+            // distribution, or too few rows to fill the GPU's row groups.
             cudaStream_t st = static_cast<cudaStream_t>(stream);
             int hmax = 0;
             cudaError_t e = cudaMemsetAsync(h->d_scratch, 0, sizeof(int), st);
@@ -398,8 +427,11 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) return cuda_fail(h, e, "plan: max row length");
             h->max_row = hmax;
-            const double fair = (double)h->nnz / (double)(kNumSMs * 32);
-            if ((double)hmax > fair && (double)hmax > 8.0 * d) pick = SPMM_ALGO_MERGE;
+            const bool skewed = (double)hmax > 16.0 * d && hmax >= 1024;
+            const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true);
+            const long long groups = (long long)num_sms() * 2 * TE_CWARPS * (32 / rc.G);  // resident row groups
+            const bool few_rows = h->m < 2 * groups;
+            pick = (skewed || few_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
         }
     }
     h->chosen = pick;
@@ -417,10 +449,10 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         // row tiles of R rows sized so a typical tile's nonzeros fit the staged shared-memory slice
         const double dd = std::max(1.0, d);
         int R = 1;
-        while (R * 2 <= 4096 && R * 2 * dd <= 2048.0) R *= 2;
+        while (R * 2 <= 4096 && R * 2 * dd <= (double)RS_TILE_NNZ) R *= 2;
         R = std::max(16, std::min(R, 1024));
         h->rows_per_tile = R;
-        long long z = (long long)std::ceil(2.0 * R * dd);
+        long long z = (long long)std::ceil(RS_ZF / 10.0 * R * dd);
         z = std::max<long long>(1024, std::min<long long>(z, 8192));
         h->capz = (int)(((z + 3) & ~3LL) + 8);
         h->num_ctas = (h->m + R - 1) / R;

@@ -71,10 +71,11 @@ struct TileInfo {
 __host__ __device__ inline size_t te_buf_bytes(int capr, int capz, int elem) {
     return (size_t)capr * 4 + (size_t)capz * 4 + (size_t)capz * elem + 64;
 }
-__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n, int stages) {
+// nw = merge workers per CTA (consumer warps x row groups per warp)
+__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n, int stages, int nw) {
     return stages * te_buf_bytes(capr, capz, elem) + 16 * TE_MAX_STAGES /*barriers*/ +
-           (size_t)(TE_CWARPS + 1) * n * elem + (size_t)(TE_CWARPS + 1) * 8 + 64 +
-           (size_t)stages * TE_CWARPS * n * elem + (size_t)stages * TE_CWARPS * 8 + stages * 4 + 64;
+           (size_t)(nw + 1) * n * elem + (size_t)(nw + 1) * 8 + 64 +
+           (size_t)stages * nw * n * elem + (size_t)stages * nw * 8 + stages * 4 + 64;
 }
 
 // stage global src[begin, end) (4-byte elements, arr_len elements in the array) at dst; returns the
@@ -170,13 +171,14 @@ k_tile(const TileParams P) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * bufb);
     uint64_t* empty = full + TE_MAX_STAGES;
     T* Cw = reinterpret_cast<T*>(smem + NS * bufb + 16 * TE_MAX_STAGES);                 // [W+1][n] worker carries
-    int* Crow = reinterpret_cast<int*>(Cw + (size_t)(TE_CWARPS + 1) * n);  // [W+1]
-    int* Cflag = Crow + (TE_CWARPS + 1);                                 // [W+1]
+    constexpr int NWK = TE_CWARPS * (32 / G);  // merge workers per CTA
+    int* Crow = reinterpret_cast<int*>(Cw + (size_t)(NWK + 1) * n);  // [NWK+1]
+    int* Cflag = Crow + (NWK + 1);                                   // [NWK+1]
     // per-stage worker carry slots for the barrier-free resolution of single-tile ranges
-    T* CwS = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(Cflag + (TE_CWARPS + 1)) + 64);  // [S][W][n]
-    int* CrowS = reinterpret_cast<int*>(CwS + (size_t)NS * TE_CWARPS * n);                   // [S][W]
-    int* CflagS = CrowS + NS * TE_CWARPS;                                                     // [S][W]
-    int* Ccnt = CflagS + NS * TE_CWARPS;                                                      // [S]
+    T* CwS = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(Cflag + (NWK + 1)) + 64);  // [S][NWK][n]
+    int* CrowS = reinterpret_cast<int*>(CwS + (size_t)NS * NWK * n);                   // [S][NWK]
+    int* CflagS = CrowS + NS * NWK;                                                     // [S][NWK]
+    int* Ccnt = CflagS + NS * NWK;                                                      // [S]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -342,8 +344,8 @@ k_tile(const TileParams P) {
     };
 
     if (MODE == MODE_MERGE && threadIdx.x == 0) {
-        Crow[TE_CWARPS] = -1;
-        Cflag[TE_CWARPS] = 0;
+        Crow[NWK] = -1;
+        Cflag[NWK] = 0;
         for (int s = 0; s < NS; ++s) Ccnt[s] = 0;
     }
     if (MODE == MODE_MERGE) named_bar_sync(1, TE_CONSUMERS);
@@ -460,10 +462,12 @@ k_tile(const TileParams P) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[b]);
         } else {
-            // ---------------- Algorithm II: merge-path items, one worker per warp ----------------
+            // ---------------- Algorithm II: merge-path items; a worker = a warp (G = 32) or, for
+            // small n, a group of G lanes (32/G independent workers per warp, lane folding) ----------
             const int rs = inf.rs, zs = inf.zs, re = inf.re, ze = inf.ze;
             const int L = (re - rs) + (ze - zs);
-            const int per = (L + TE_CWARPS - 1) / TE_CWARPS;
+            const int wid = warp * S + slot;  // worker id, ascending along the merge path
+            const int per = (L + NWK - 1) / NWK;
             const int* Eb = E + 1 - inf.ebase;  // Eb[x] = ro[x+1] (row end of row x)
             auto search = [&](int d) -> int {
                 const int D = rs + zs + d;
@@ -474,7 +478,7 @@ k_tile(const TileParams P) {
                 }
                 return lo;
             };
-            const int d0 = min(warp * per, L), d1 = min((warp + 1) * per, L);
+            const int d0 = min(wid * per, L), d1 = min((wid + 1) * per, L);
             const int ia = search(d0), ja = rs + zs + d0 - ia;
             const int ib = search(d1), jb = rs + zs + d1 - ib;
 
@@ -483,13 +487,13 @@ k_tile(const TileParams P) {
             for (int k = 1; k < NA; ++k) accs[k].reset();
             Acc<T, SR, VEC, NV>& acc = accs[0];
             bool dirty = false;
-            if (warp == 0 && !(inf.flags & 1) && Cflag[TE_CWARPS]) {  // carry-in from the previous sub-tile
+            if (wid == 0 && !(inf.flags & 1) && Cflag[NWK]) {  // carry-in from the previous sub-tile
 #pragma unroll
                 for (int v = 0; v < NV; ++v)
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) {
                         const int cc = gl * VEC + v * G * VEC + x;
-                        acc.v[v][x] = (cc < n) ? Cw[TE_CWARPS * n + cc] : R::id();
+                        acc.v[v][x] = (cc < n) ? Cw[NWK * n + cc] : R::id();
                     }
                 dirty = true;
             } else {
@@ -512,6 +516,7 @@ k_tile(const TileParams P) {
                 ++r;
                 e = (r < m) ? Eb[r] : 0x7fffffff;
             };
+          if constexpr (G == 32) {
 #ifndef MG_PF
 #define MG_PF 0
 #endif
@@ -575,6 +580,50 @@ k_tile(const TileParams P) {
                 q += cnt;
             }
             while (r < ib) flush();
+          } else {
+            // folded workers (small n): each G-lane group walks its own equal share of the merge path
+            // item by item -- nonzero (gather + FMA) or row end (store C row, reset) -- all groups of
+            // the warp in lock-step (equal item counts), item types predicated instead of branched
+            constexpr int UF = (U < 8) ? U : 8;
+            const int items = d1 - d0;
+            const int steps = __reduce_max_sync(FULL, items);
+            const uint32_t col_s = smem_u32(COL) - 4u * (uint32_t)inf.zbase;
+            const uint32_t val_s = smem_u32(VAL) - 4u * (uint32_t)inf.zbase;
+            for (int t0 = 0; t0 < steps; t0 += UF) {
+                unsigned bv[UF][NV][VEC];
+                unsigned au[UF];
+                bool isn[UF], isr[UF];
+                const int rstart = r;
+#pragma unroll
+                for (int u = 0; u < UF; ++u) {
+                    const bool active = t0 + u < items;
+                    isn[u] = active && (q < e);   // rows first on ties: row r ends before nonzero q if e <= q
+                    isr[u] = active && !isn[u];
+                    const unsigned c = lds_pred(col_s + 4u * (uint32_t)q, isn[u]);
+                    au[u] = lds_pred(val_s + 4u * (uint32_t)q, isn[u]);
+                    gather(bv[u], (int)c, isn[u]);
+                    q += isn[u] ? 1 : 0;
+                    if (isr[u]) {
+                        ++r;
+                        e = (r < m) ? Eb[r] : 0x7fffffff;
+                    }
+                }
+                int rr = rstart;
+#pragma unroll
+                for (int u = 0; u < UF; ++u) {
+                    if (isn[u]) {
+                        acc.mac(from_bits<T>(au[u]), bv[u]);
+                        dirty = true;
+                    }
+                    if (isr[u]) {
+                        store_row(rr, acc, true);
+                        acc.reset();
+                        dirty = false;
+                        ++rr;
+                    }
+                }
+            }
+          }
             collapse();
 
             // ---- carry resolution (Alg. 1 line 22): sums worker partials of the same row in ascending
@@ -585,14 +634,14 @@ k_tile(const TileParams P) {
 #pragma unroll
                 for (int t2 = 0; t2 < 4; ++t2) open[t2] = R::id();
                 int w = 0;
-                while (w < TE_CWARPS) {
+                while (w < NWK) {
                     const int row = srow[w];
                     bool any = false;
                     T sacc[4];
 #pragma unroll
                     for (int t2 = 0; t2 < 4; ++t2) sacc[t2] = R::id();
                     int w2 = w;
-                    while (w2 < TE_CWARPS && srow[w2] == row) {
+                    while (w2 < NWK && srow[w2] == row) {
                         if (sflag[w2]) {
                             any = true;
 #pragma unroll
@@ -632,14 +681,14 @@ k_tile(const TileParams P) {
                 }
             };
             auto publish = [&](T* slots, int* srow, int* sflag) {
-                if (lane == 0) { srow[warp] = ib; sflag[warp] = dirty ? 1 : 0; }
+                if (gl == 0) { srow[wid] = ib; sflag[wid] = dirty ? 1 : 0; }
                 if (dirty) {
 #pragma unroll
                     for (int v = 0; v < NV; ++v)
 #pragma unroll
                         for (int x = 0; x < VEC; ++x) {
                             const int cc = gl * VEC + v * G * VEC + x;
-                            if (colok[v]) slots[warp * n + cc] = acc.v[v][x];
+                            if (colok[v] && cc < n) slots[wid * n + cc] = acc.v[v][x];
                         }
                 }
             };
@@ -647,9 +696,9 @@ k_tile(const TileParams P) {
             if ((inf.flags & 3) == 3) {
                 // whole range in one tile (2-D merge path): barrier-free -- the last worker to finish
                 // resolves the carries, the others move straight on to their next tile
-                T* slots = CwS + (size_t)b * TE_CWARPS * n;
-                int* srow = CrowS + b * TE_CWARPS;
-                int* sflag = CflagS + b * TE_CWARPS;
+                T* slots = CwS + (size_t)b * NWK * n;
+                int* srow = CrowS + b * NWK;
+                int* sflag = CflagS + b * NWK;
                 publish(slots, srow, sflag);
                 __syncwarp();
                 int last = 0;
@@ -683,12 +732,12 @@ k_tile(const TileParams P) {
                 bool open_any;
                 resolve(Cw, Crow, Cflag, open, open_any);
                 __syncwarp();
-                if (lane == 0) { Crow[TE_CWARPS] = re; Cflag[TE_CWARPS] = open_any ? 1 : 0; }
+                if (lane == 0) { Crow[NWK] = re; Cflag[NWK] = open_any ? 1 : 0; }
                 if (open_any) {
 #pragma unroll
                     for (int t2 = 0; t2 < 4; ++t2) {
                         const int cc = lane + 32 * t2;
-                        if (cc < n) Cw[TE_CWARPS * n + cc] = open[t2];
+                        if (cc < n) Cw[NWK * n + cc] = open[t2];
                     }
                 }
                 if (inf.flags & 2) write_global_carry(open, open_any);
