@@ -119,6 +119,25 @@ __device__ __forceinline__ const char* opaque_ptr(const char* p) {
     return q;
 }
 
+// Ampere-style async copy global -> shared (LDGSTS), 4/8/16 bytes, tracked per thread in groups
+template <int BYTES> __device__ __forceinline__ void cp_async(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int VEC> __device__ __forceinline__ void lds_vec(unsigned (&o)[VEC], uint32_t saddr);
+template <> __device__ __forceinline__ void lds_vec<1>(unsigned (&o)[1], uint32_t a) {
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(o[0]) : "r"(a));
+}
+template <> __device__ __forceinline__ void lds_vec<2>(unsigned (&o)[2], uint32_t a) {
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(o[0]), "=r"(o[1]) : "r"(a));
+}
+template <> __device__ __forceinline__ void lds_vec<4>(unsigned (&o)[4], uint32_t a) {
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "r"(a));
+}
+
 // d = a * b + c on two packed fp32 lanes (sm_100 FFMA2)
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
     uint64_t d;

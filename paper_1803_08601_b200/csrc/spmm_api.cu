@@ -48,7 +48,7 @@ constexpr int kNumSMs = 148;
 #define RS_U 8
 #endif
 #ifndef MG_U
-#define MG_U 16
+#define MG_U 8
 #endif
 #ifndef MG_FOLD
 #define MG_FOLD 0  // merge with lane-folded workers for n <= 16 (experimental; slower on B200 so far)
@@ -63,7 +63,7 @@ constexpr int kNumSMs = 148;
 #define RS_ZF 12  // row split: staged capacity = RS_ZF/10 x the tile's expected nonzeros
 #endif
 #ifndef MG_SMEM_BUDGET
-#define MG_SMEM_BUDGET 75000  // bytes of staged CSR tiles per merge CTA (stages = budget / tile bytes)
+#define MG_SMEM_BUDGET 50000  // bytes of staged CSR tiles per merge CTA (stages = budget / tile bytes)
 #endif
 #ifndef MG_ITEMS
 #define MG_ITEMS 2048
@@ -174,9 +174,15 @@ int num_sms() {
 }
 
 template <typename T, int SR, int MODE, int V, int G, int NV, int U>
-cudaError_t launch_tile(const TileParams& P, cudaStream_t st) {
+cudaError_t launch_tile(TileParams P, cudaStream_t st) {
     auto kfn = k_tile<T, SR, MODE, V, G, NV, U>;
-    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G));
+    size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G));
+    if (MODE == MODE_MERGE && G == 32) {  // + per-warp cp.async rings of gathered B rows
+        const int SB = 32 * V * NV * (int)sizeof(T);
+        smem = (smem + 15) & ~(size_t)15;
+        P.ring_off = (int)smem;
+        smem += (size_t)TE_CWARPS * mg_ring_slots(SB) * SB;
+    }
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
