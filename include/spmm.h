@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define SPMM_ABI_VERSION 1
+#define SPMM_ABI_VERSION 2
 
 typedef struct spmm_csr_s* spmm_csr_t;
 
@@ -63,6 +63,7 @@ enum { SPMM_FLAG_VALIDATE = 1u };                                       /* one c
 
 typedef enum { SPMM_POLICY_AUTO = 0, SPMM_POLICY_PAPER = 1 } spmm_policy;
 typedef enum { SPMM_PARTITION_MERGE_PATH = 0, SPMM_PARTITION_NONZERO_SPLIT = 1 } spmm_partition;
+typedef enum { SPMM_PAIRING_AUTO = 0, SPMM_PAIRING_OFF = 1, SPMM_PAIRING_ON = 2 } spmm_row_pairing;
 
 /* Optional planner knobs (spmm_csr_plan_ex).  Zero-initialised = defaults. */
 typedef struct {
@@ -76,7 +77,13 @@ typedef struct {
                                 (PAPER.md:80, :89).                                                  */
     int32_t items_per_cta;   /* merge-path items (rows + nonzeros) per CTA; 0 = default (2048).
                                 Must be a multiple of 256 in [256, 4096].                           */
-    int32_t reserved[5];     /* must be zero */
+    int32_t row_pairing;     /* spmm_row_pairing for the row-split kernel (B200 extension):
+                                AUTO (0) = measure at plan time (one O(nnz) device pass + stream sync)
+                                how many B-row gathers pairing adjacent rows would share and pair
+                                when >= 25% of the nonzeros share (never under policy PAPER); OFF (1) =
+                                one row per lane group, the paper's row split; ON (2)
+                                = always pair.  The result is C = AB either way.                     */
+    int32_t reserved[4];     /* must be zero */
 } spmm_plan_opts;
 
 /* Read-only description of the current plan (spmm_csr_get_plan_info). */
@@ -91,7 +98,7 @@ typedef struct {
     int32_t num_ctas;        /* CTAs of the compute kernel */
     int32_t items_per_cta;   /* merge only */
     int32_t launches_per_execute;  /* kernels one execute() enqueues (row split 1, merge 3) */
-    int32_t reserved0;
+    int32_t row_pairing;     /* 1 if the row-split kernel runs on row pairs (see spmm_plan_opts) */
     size_t workspace_bytes;
 } spmm_plan_info;
 

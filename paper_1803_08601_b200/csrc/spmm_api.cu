@@ -34,8 +34,12 @@ struct spmm_csr_s {
     int32_t items = 2048;
     int32_t rows_per_tile = 128;  // row split: rows per tile
     int32_t capz = 4104;          // row split: staged nonzeros per tile (+8 slack)
+    int32_t capb = 0;             // row split: bytes of staged B row span per stage (0 = gather B from global)
+    double bspan_compact = -1.0;  // fraction of nonzeros in row tiles whose B span is compact (plan-time)
     size_t ws_bytes = 0;
-    int* d_scratch = nullptr;  // 16 bytes: plan-time reduction / validation flags
+    bool pairing = false;      // row split on row pairs (spmm_plan_opts.row_pairing)
+    double pair_shared = -1.0; // fraction of nonzeros whose B row a pair shares (plan-time measurement)
+    int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
     int32_t nev = 0;
     std::string err;
@@ -52,6 +56,9 @@ constexpr int kNumSMs = 148;
 #endif
 #ifndef MG_FOLD
 #define MG_FOLD 0  // merge with lane-folded workers for n <= 16 (experimental; slower on B200 so far)
+#endif
+#ifndef TE_CARVE
+#define TE_CARVE 1  // request the minimal shared-memory carveout (maximal L1) for the resident CTAs
 #endif
 #ifndef RS_STAGES
 #define RS_STAGES 3
@@ -71,6 +78,25 @@ constexpr int kNumSMs = 148;
 constexpr int kDefaultItems = MG_ITEMS;
 constexpr int kRowsplitU = RS_U;
 constexpr int kMergeU = MG_U;
+#ifndef RSP_U
+#define RSP_U 4
+#endif
+constexpr int kPairU = RSP_U;
+#ifndef RS_BSTAGE
+#define RS_BSTAGE 1  // row split: stage compact B row spans into shared memory with TMA (plan-time measured)
+#endif
+#ifndef RS_HALO_F
+#define RS_HALO_F 2.0
+#endif
+#ifndef RS_BSTAGE_MIN
+#define RS_BSTAGE_MIN 0.5  // stage B when at least this fraction of the nonzeros lies in compact tiles
+#endif
+#ifndef RS_BSTAGE_SMEM
+#define RS_BSTAGE_SMEM 110000  // shared-memory budget per CTA with B staging (2 CTAs per SM)
+#endif
+#ifndef RSP_MIN_SHARE
+#define RSP_MIN_SHARE 2.0  // row_pairing AUTO: pair when this fraction of nonzeros shares a B row (> 1: never)
+#endif
 
 spmm_status fail(spmm_csr_t h, spmm_status s, const std::string& msg) {
     if (h) h->err = msg;
@@ -97,6 +123,67 @@ __global__ void k_max_row(const int* __restrict__ ro, long long m, int* __restri
         best = max(best, ro[i + 1] - ro[i]);
     best = __reduce_max_sync(FULL, best);
     if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// Row-pair sharing measurement for spmm_plan_opts.row_pairing = AUTO: for every pair of rows (2i, 2i+1)
+// count the entries of row 2i+1 whose B row the pair kernel (tile.cuh) would share with row 2i, using the
+// kernel's own rule (entry j of Q pairs with entry j + delta of L, delta = #{L cols < Q's first col},
+// when the columns are equal; pairs with a row longer than 32 are not paired).  out[0] += shared,
+// out[1] += nonzeros of all pairs.
+__global__ void k_pair_share(const int* __restrict__ ro, const int* __restrict__ col, long long m,
+                             unsigned long long* __restrict__ out) {
+    unsigned long long shared = 0, total = 0;
+    const long long pairs = (m + 1) / 2;
+    for (long long pi = (long long)blockIdx.x * blockDim.x + threadIdx.x; pi < pairs;
+         pi += (long long)gridDim.x * blockDim.x) {
+        const long long l = 2 * pi;
+        const int sL = ro[l], eL = ro[l + 1];
+        const int eQ = (l + 1 < m) ? ro[l + 2] : eL;
+        total += (unsigned long long)(eQ - sL);
+        const int lenL = eL - sL, lenQ = eQ - eL;
+        if (lenL > 32 || lenQ > 32 || lenQ == 0) continue;
+        const int q0 = col[eL];
+        int delta = 0;
+        for (int i = 0; i < lenL; ++i) delta += (col[sL + i] < q0) ? 1 : 0;
+        for (int j = 0; j < lenQ; ++j) {
+            const int i = j + delta;
+            if (i < lenL && col[sL + i] == col[eL + j]) ++shared;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        shared += __shfl_down_sync(FULL, shared, o);
+        total += __shfl_down_sync(FULL, total, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], shared);
+        atomicAdd(&out[1], total);
+    }
+}
+
+// B-span compactness for the row-split kernel's B staging: warp per row tile of R rows; a tile is
+// compact when its column span [lo, hi] holds at most 2 B rows per nonzero and fits capb bytes at
+// row_bytes per row.  out[0] += nonzeros of compact tiles.
+__global__ void k_tile_span(const int* __restrict__ ro, const int* __restrict__ col, long long m, int R,
+                            long long row_bytes, long long capb, unsigned long long* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long tiles = (m + R - 1) / R;
+    const long long nw = (long long)gridDim.x * (blockDim.x / 32);
+    unsigned long long acc = 0;
+    for (long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32; t < tiles; t += nw) {
+        const long long rs = t * R, re = min(m, rs + R);
+        const int zs = ro[rs], ze = ro[re];
+        int lo = 0x7fffffff, hi = -1;
+        for (int p = zs + lane; p < ze; p += 32) {
+            const int c = col[p];
+            lo = min(lo, c);
+            hi = max(hi, c);
+        }
+        lo = __reduce_min_sync(FULL, lo);
+        hi = __reduce_max_sync(FULL, hi);
+        const long long cnt = ze - zs, span = (long long)hi - lo + 1;
+        if (cnt > 0 && span <= 2 * cnt && span * row_bytes <= capb) acc += (unsigned long long)cnt;
+    }
+    if (lane == 0 && acc) atomicAdd(out, acc);
 }
 
 // flags: bit0 ro[0] != 0, bit1 decreasing offsets, bit2 ro[m] != nnz, bit3 column out of range
@@ -173,10 +260,13 @@ int num_sms() {
     return sms;
 }
 
-template <typename T, int SR, int MODE, int V, int G, int NV, int U>
+template <typename T, int SR, int MODE, int V, int G, int NV, int U, bool PAIR = false>
 cudaError_t launch_tile(TileParams P, cudaStream_t st) {
-    auto kfn = k_tile<T, SR, MODE, V, G, NV, U>;
-    size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G));
+    void (*kfn)(const TileParams);
+    if constexpr (PAIR) kfn = k_tile_pair<T, SR, V, G, NV, U>;
+    else kfn = k_tile<T, SR, MODE, V, G, NV, U>;
+    size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G), MODE == MODE_MERGE,
+                                MODE == MODE_ROWSPLIT ? P.capb : 0);
     if (MODE == MODE_MERGE && G == 32) {  // + per-warp cp.async rings of gathered B rows
         const int SB = 32 * V * NV * (int)sizeof(T);
         smem = (smem + 15) & ~(size_t)15;
@@ -189,6 +279,21 @@ cudaError_t launch_tile(TileParams P, cudaStream_t st) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, TE_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (per_sm <= 0) return cudaErrorInvalidConfiguration;
+#if TE_CARVE
+    {
+        // ask for the smallest shared-memory carveout that still fits the resident CTAs: the rest of the
+        // 228 KB unified array stays L1, which is where gathered B rows are reused (row split: every
+        // banded B row is read by 16 neighbouring rows)
+        const int want = std::min(per_sm, MODE == MODE_MERGE ? TE_MINB_MG : TE_MINB);  // pair kernels: 2 as row split
+        const size_t need = (size_t)want * (smem + 1024);
+        const int pct = (int)std::min<size_t>(100, (need * 100 + 228 * 1024 - 1) / (228 * 1024));
+        e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, TE_THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm <= 0) return cudaErrorInvalidConfiguration;
+    }
+#endif
     const long long grid = std::min<long long>(P.num_ranges, (long long)per_sm * num_sms());
     if (grid <= 0) return cudaSuccess;
     kfn<<<(unsigned)grid, TE_THREADS, smem, st>>>(P);
@@ -202,8 +307,30 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
     P.capr = h->rows_per_tile + 8;
     P.capz = h->capz;
     P.stages = RS_STAGES;
+    // B staging needs 16-byte aligned B rows (TMA bulk copy source)
+    P.capb = (h->capb > 0 && ((uintptr_t)P.B % 16) == 0 && (P.ldb_bytes % 16) == 0) ? h->capb : 0;
     mark(h, 0, st);
     cudaError_t e;
+    if (h->pairing) {
+        e = cudaErrorNotSupported;
+#ifdef RSP_WIDE
+        if (cfg.NV == 2 && cfg.G <= 8) {  // pairs: a row over twice the lanes, one vector block each
+            cfg.G *= 2;
+            cfg.NV = 1;
+        }
+#endif
+#define RSP_CASE(V, G_, NV_) \
+    case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kPairU, true>(P, st); break;
+        switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
+            RSP_CASE(4, 2, 1) RSP_CASE(4, 4, 1) RSP_CASE(4, 8, 1) RSP_CASE(4, 8, 2) RSP_CASE(4, 16, 2) RSP_CASE(4, 16, 1)
+            default: break;
+        }
+#undef RSP_CASE
+        if (e != cudaErrorNotSupported) {  // no pair instance for this vector shape: plain row split
+            mark(h, 1, st);
+            return e;
+        }
+    }
 #define RS_CASE(V, G_, NV_) \
     case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kRowsplitU>(P, st); break;
     switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
@@ -340,7 +467,7 @@ spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, 
     if (!h) return SPMM_ERR_CUDA;
     h->m = m; h->k = k; h->nnz = nnz;
     h->ro = row_offsets; h->col = col_indices; h->val = values; h->dtype = dtype;
-    cudaError_t e = cudaMalloc(&h->d_scratch, 16);
+    cudaError_t e = cudaMalloc(&h->d_scratch, 32);
     if (e != cudaSuccess) { delete h; return SPMM_ERR_CUDA; }
     if ((flags & SPMM_FLAG_VALIDATE) && m > 0) {
         cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -394,8 +521,10 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     if (sr != SPMM_PLUS_TIMES && sr != SPMM_MIN_PLUS) return fail(h, SPMM_ERR_INVALID_ARG, "bad semiring");
     spmm_plan_opts o{};
     if (opts) o = *opts;
-    for (int i = 0; i < 5; ++i)
+    for (int i = 0; i < 4; ++i)
         if (o.reserved[i] != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
+    if (o.row_pairing != SPMM_PAIRING_AUTO && o.row_pairing != SPMM_PAIRING_OFF && o.row_pairing != SPMM_PAIRING_ON)
+        return fail(h, SPMM_ERR_INVALID_ARG, "bad row_pairing");
     if (o.policy != SPMM_POLICY_AUTO && o.policy != SPMM_POLICY_PAPER) return fail(h, SPMM_ERR_INVALID_ARG, "bad policy");
     if (o.partition != SPMM_PARTITION_MERGE_PATH && o.partition != SPMM_PARTITION_NONZERO_SPLIT)
         return fail(h, SPMM_ERR_INVALID_ARG, "bad partition");
@@ -409,6 +538,10 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     h->opts = o;
     h->items = items;
     h->max_row = -1;
+    h->pairing = false;
+    h->pair_shared = -1.0;
+    h->capb = 0;
+    h->bspan_compact = -1.0;
     const double d = h->m > 0 ? (double)h->nnz / (double)h->m : 0.0;  // PAPER.md:267, mean row length
     spmm_algo pick = algo;
     if (algo == SPMM_ALGO_AUTO) {
@@ -457,11 +590,72 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         int R = 1;
         while (R * 2 <= 4096 && R * 2 * dd <= (double)RS_TILE_NNZ) R *= 2;
         R = std::max(16, std::min(R, 1024));
+        auto capz_for = [&](int rows) {
+            long long z = (long long)std::ceil(RS_ZF / 10.0 * rows * dd);
+            z = std::max<long long>(1024, std::min<long long>(z, 8192));
+            return (int)(((z + 3) & ~3LL) + 8);
+        };
         h->rows_per_tile = R;
-        long long z = (long long)std::ceil(RS_ZF / 10.0 * R * dd);
-        z = std::max<long long>(1024, std::min<long long>(z, 8192));
-        h->capz = (int)(((z + 3) & ~3LL) + 8);
+        h->capz = capz_for(R);
+        h->capb = 0;
+        h->bspan_compact = -1.0;
+        if (RS_BSTAGE && h->nnz > 0) {
+            // B staging: smaller tiles whose B row span (R_b rows + the band around them)
+            // fits a per-stage shared-memory slot next to the CSR slice, 3 stages x 2 CTAs per SM
+            const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
+            const long long row_bytes = (long long)((n * elem + 15) & ~(size_t)15);
+            const int halo = std::max(16, (int)std::ceil(RS_HALO_F * dd));  // B rows beyond R the span may need
+            int Rb = R;
+            long long capb = 0;
+            while (true) {
+                capb = ((long long)(Rb + halo) * row_bytes + 15) & ~15LL;
+                const long long stage = (long long)te_buf_bytes(Rb + 8, capz_for(Rb), (int)elem, (int)capb);
+                if (RS_STAGES * stage <= RS_BSTAGE_SMEM || Rb <= 16) break;
+                Rb /= 2;
+            }
+            if (RS_STAGES * (long long)te_buf_bytes(Rb + 8, capz_for(Rb), (int)elem, (int)capb) <= RS_BSTAGE_SMEM) {
+                cudaStream_t st = static_cast<cudaStream_t>(stream);
+                unsigned long long cnt = 0;
+                unsigned long long* dc = reinterpret_cast<unsigned long long*>(h->d_scratch + 4);
+                cudaError_t e = cudaMemsetAsync(dc, 0, sizeof(cnt), st);
+                if (e == cudaSuccess) {
+                    const long long tiles = (h->m + Rb - 1) / Rb;
+                    const int grid = (int)std::min<long long>((tiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA, 8LL * kNumSMs);
+                    k_tile_span<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, Rb, row_bytes, capb, dc);
+                    e = cudaGetLastError();
+                }
+                if (e == cudaSuccess) e = cudaMemcpyAsync(&cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) return cuda_fail(h, e, "plan: B span");
+                h->bspan_compact = (double)cnt / (double)h->nnz;
+                if (h->bspan_compact >= RS_BSTAGE_MIN) {
+                    h->rows_per_tile = Rb;
+                    h->capz = capz_for(Rb);
+                    h->capb = (int)capb;
+                }
+            }
+        }
+        R = h->rows_per_tile;
         h->num_ctas = (h->m + R - 1) / R;
+        if (o.row_pairing == SPMM_PAIRING_ON) {
+            h->pairing = true;
+        } else if (o.row_pairing == SPMM_PAIRING_AUTO && o.policy == SPMM_POLICY_AUTO && h->nnz > 0 && h->m > 1) {
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            unsigned long long cnt[2] = {0, 0};
+            unsigned long long* dc = reinterpret_cast<unsigned long long*>(h->d_scratch + 4);
+            cudaError_t e = cudaMemsetAsync(dc, 0, 2 * sizeof(unsigned long long), st);
+            if (e == cudaSuccess) {
+                const long long pairs = (h->m + 1) / 2;
+                const int grid = (int)std::min<long long>((pairs + THREADS - 1) / THREADS, 8LL * kNumSMs);
+                k_pair_share<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, dc);
+                e = cudaGetLastError();
+            }
+            if (e == cudaSuccess) e = cudaMemcpyAsync(cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_fail(h, e, "plan: row-pair sharing");
+            h->pair_shared = cnt[1] ? (double)cnt[0] / (double)cnt[1] : 0.0;
+            h->pairing = h->pair_shared >= RSP_MIN_SHARE;
+        }
     }
     h->planned = true;
     if (workspace_bytes) *workspace_bytes = h->ws_bytes;
@@ -487,6 +681,7 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
     out->num_ctas = (int32_t)h->num_ctas;
     out->items_per_cta = h->chosen == SPMM_ALGO_MERGE ? h->items : 0;
     out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : 1);
+    out->row_pairing = (h->chosen == SPMM_ALGO_ROWSPLIT && h->pairing) ? 1 : 0;
     out->workspace_bytes = h->ws_bytes;
     return SPMM_OK;
 }

@@ -62,6 +62,7 @@ struct TileParams {
     unsigned pf_bytes;  // bytes of each B row to prefetch into L2 ahead of the consumers (0 = off)
     int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
     int ring_off;       // merge: byte offset of the per-warp B-row rings in dynamic shared memory
+    int capb;           // rowsplit: bytes per stage for the tile's B row span (0 = B is gathered from global)
 };
 
 // tile descriptor written by the producer next to the staged data
@@ -69,16 +70,22 @@ struct TileInfo {
     int rs, zs, re, ze;  // merge-path state at tile start / end (rowsplit: zs = ro[rs], ze = ro[re])
     int ebase, zbase;    // global index of E[0] and of COL[0]/VAL[0]
     int range;           // partition range (merge) / row tile (rowsplit)
-    int flags;           // 1 first sub-tile of range, 2 last sub-tile, 4 staged, 8 done
+    int flags;           // 1 first sub-tile of range, 2 last sub-tile, 4 staged, 8 done, 16 B span staged
+    int blo;             // flags & 16: B row held at the start of the staged B span
 };
 
-__host__ __device__ inline size_t te_buf_bytes(int capr, int capz, int elem) {
-    return (size_t)capr * 4 + (size_t)capz * 4 + (size_t)capz * elem + 64;
+// one pipeline stage: row offsets | column indices | values | TileInfo (64 B) | B row span (capb bytes)
+__host__ __device__ inline size_t te_buf_bytes(int capr, int capz, int elem, int capb = 0) {
+    return (size_t)capr * 4 + (size_t)capz * 4 + (size_t)capz * elem + 64 + (size_t)capb;
 }
-// nw = merge workers per CTA (consumer warps x row groups per warp)
-__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n, int stages, int nw) {
-    return stages * te_buf_bytes(capr, capz, elem) + 16 * TE_MAX_STAGES /*barriers*/ +
-           (size_t)(nw + 1) * n * elem + (size_t)(nw + 1) * 8 + 64 +
+constexpr int TE_BAR_BYTES = 24 * TE_MAX_STAGES;  // full / empty / csr-landed mbarriers
+// nw = merge workers per CTA (consumer warps x row groups per warp); row split needs no carry slots,
+// and every byte of shared memory it does not claim stays L1 (unified carveout) for B-row reuse
+__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n, int stages, int nw, bool merge,
+                                                int capb = 0) {
+    const size_t base = stages * te_buf_bytes(capr, capz, elem, capb) + TE_BAR_BYTES;
+    if (!merge) return base;
+    return base + (size_t)(nw + 1) * n * elem + (size_t)(nw + 1) * 8 + 64 +
            (size_t)stages * nw * n * elem + (size_t)stages * nw * 8 + stages * 4 + 64;
 }
 
@@ -116,6 +123,22 @@ template <> __device__ __forceinline__ void ldg_pred<4>(unsigned (&o)[4], const 
     asm volatile("{.reg .pred q; setp.ne.b32 q, %5, 0; mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;"
                  " @q ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];}"
                  : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p), "r"((int)pred));
+}
+
+// predicated vector load from shared memory (o = 0 if !pred; no access)
+template <int VEC> __device__ __forceinline__ void lds_vpred(unsigned (&o)[VEC], uint32_t a, bool pred);
+template <> __device__ __forceinline__ void lds_vpred<1>(unsigned (&o)[1], uint32_t a, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; mov.b32 %0, 0; @q ld.shared.b32 %0, [%1];}"
+                 : "=r"(o[0]) : "r"(a), "r"((int)pred));
+}
+template <> __device__ __forceinline__ void lds_vpred<2>(unsigned (&o)[2], uint32_t a, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %3, 0; mov.b32 %0, 0; mov.b32 %1, 0; @q ld.shared.v2.b32 {%0, %1}, [%2];}"
+                 : "=r"(o[0]), "=r"(o[1]) : "r"(a), "r"((int)pred));
+}
+template <> __device__ __forceinline__ void lds_vpred<4>(unsigned (&o)[4], uint32_t a, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %5, 0; mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;"
+                 " @q ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];}"
+                 : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "r"(a), "r"((int)pred));
 }
 
 #ifndef MG_RING_BYTES
@@ -178,23 +201,24 @@ template <typename T, int SR, int VEC, int NV> struct Acc {
     }
 };
 
-template <typename T, int SR, int MODE, int VEC, int G, int NV, int U>
-__global__ void __launch_bounds__(TE_THREADS, MODE == MODE_MERGE ? TE_MINB_MG : TE_MINB)
-k_tile(const TileParams P) {
+template <typename T, int SR, int MODE, int VEC, int G, int NV, int U, bool PAIR>
+__device__ __forceinline__ void tile_body(const TileParams& P) {
     using R = Ring<T, SR>;
     extern __shared__ __align__(128) unsigned char smem[];
     const int capr = P.capr, capz = P.capz, n = P.n, m = P.m;
-    const size_t bufb = te_buf_bytes(capr, capz, (int)sizeof(T));
+    const size_t bufb = te_buf_bytes(capr, capz, (int)sizeof(T), MODE == MODE_ROWSPLIT ? P.capb : 0);
     auto E_of = [&](int b) { return reinterpret_cast<int*>(smem + b * bufb); };
     auto COL_of = [&](int b) { return reinterpret_cast<int*>(smem + b * bufb + (size_t)capr * 4); };
     auto VAL_of = [&](int b) { return reinterpret_cast<T*>(smem + b * bufb + (size_t)capr * 4 + (size_t)capz * 4); };
     auto INFO_of = [&](int b) {
         return reinterpret_cast<TileInfo*>(smem + b * bufb + (size_t)capr * 4 + (size_t)capz * (4 + sizeof(T)));
     };
+    auto BS_of = [&](int b) { return smem + b * bufb + (size_t)capr * 4 + (size_t)capz * (4 + sizeof(T)) + 64; };
     const int NS = P.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * bufb);
     uint64_t* empty = full + TE_MAX_STAGES;
-    T* Cw = reinterpret_cast<T*>(smem + NS * bufb + 16 * TE_MAX_STAGES);                 // [W+1][n] worker carries
+    uint64_t* landed = empty + TE_MAX_STAGES;  // rowsplit + B staging: the tile's CSR slice has landed
+    T* Cw = reinterpret_cast<T*>(smem + NS * bufb + TE_BAR_BYTES);                 // [W+1][n] worker carries
     constexpr int NWK = TE_CWARPS * (32 / G);  // merge workers per CTA
     int* Crow = reinterpret_cast<int*>(Cw + (size_t)(NWK + 1) * n);  // [NWK+1]
     int* Cflag = Crow + (NWK + 1);                                   // [NWK+1]
@@ -211,6 +235,7 @@ k_tile(const TileParams P) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], TE_CWARPS);
+            mbar_init(&landed[s], 1);
         }
         fence_mbar_init();
     }
@@ -224,6 +249,15 @@ k_tile(const TileParams P) {
             b = i % NS;
             if (i >= NS) {
                 while (!mbar_try_wait(&empty[b], ((i / NS) - 1) & 1)) __nanosleep(64);
+            }
+        };
+        auto prefetch_span = [&](int lo, long long span) {
+            const char* base = static_cast<const char*>(P.B) + (size_t)(unsigned)lo * P.ldb_bytes;
+            const long long bytes = (span - 1) * (long long)P.ldb_bytes + P.pf_bytes;
+            constexpr long long CHUNK = 16384;
+            for (long long off = (long long)lane * CHUNK; off < bytes; off += 32 * CHUNK) {
+                const long long len = min(CHUNK, bytes - off);
+                prefetch_l2_bulk(base + off, (uint32_t)(len & ~15LL));
             }
         };
         // L2 prefetch of the B rows a staged tile will gather, when the tile's columns are clustered
@@ -247,14 +281,51 @@ k_tile(const TileParams P) {
             hi = __reduce_max_sync(FULL, hi);
             const long long span = (long long)hi - lo + 1;
             if (span > 2LL * cnt) return;  // scattered columns: nothing compact to prefetch
-            const char* base = static_cast<const char*>(P.B) + (size_t)(unsigned)lo * P.ldb_bytes;
-            const long long bytes = (span - 1) * (long long)P.ldb_bytes + P.pf_bytes;
-            constexpr long long CHUNK = 16384;
-            for (long long off = (long long)lane * CHUNK; off < bytes; off += 32 * CHUNK) {
-                const long long len = min(CHUNK, bytes - off);
-                prefetch_l2_bulk(base + off, (uint32_t)(len & ~15LL));
-            }
+            prefetch_span(lo, span);
         };
+        // B staging (row split, P.capb > 0): once tile ti's CSR slice has landed (`landed` barrier), the
+        // producer finds the tile's B row span [lo, hi] and, when it is compact (at most 2 rows per
+        // nonzero) and fits the stage, copies those B rows into shared memory with one TMA bulk copy
+        // that completes on the consumers' `full` barrier.  The consumers then gather B rows from
+        // shared memory (no DRAM / L2 latency left in their dependency chain); other tiles keep the
+        // global gathers (+ L2 prefetch when the span is compact but too large).
+        const uint64_t polb = policy_evict_last();
+        auto finish_tile = [&](int pb, int ti) {
+            mbar_wait(&landed[pb], (ti / NS) & 1);
+            TileInfo* ip = INFO_of(pb);
+            const TileInfo pi = *ip;
+            uint32_t btx = 0;
+            const int cnt = pi.ze - pi.zs;
+            if ((pi.flags & 4) && cnt > 0) {
+                const int* pc = COL_of(pb) + (pi.zs - pi.zbase);
+                int lo = 0x7fffffff, hi = -1;
+                for (int t = lane; t < cnt; t += 32) {
+                    const int c = pc[t];
+                    lo = min(lo, c);
+                    hi = max(hi, c);
+                }
+                lo = __reduce_min_sync(FULL, lo);
+                hi = __reduce_max_sync(FULL, hi);
+                const long long span = (long long)hi - lo + 1;
+                const long long bytes = span * (long long)P.ldb_bytes;
+                if (span <= 2LL * cnt && bytes <= P.capb) {
+                    if (lane == 0) {
+                        fence_proxy_async_smem();
+                        tma_load_1d(BS_of(pb), static_cast<const char*>(P.B) + (size_t)(unsigned)lo * P.ldb_bytes,
+                                    (uint32_t)bytes, &full[pb], polb);
+                        ip->flags = pi.flags | 16;
+                        ip->blo = lo;
+                    }
+                    btx = (uint32_t)bytes;
+                } else if (span <= 2LL * cnt && P.pf_bytes) {
+                    prefetch_span(lo, span);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&full[pb], btx);
+        };
+        const bool bstage = MODE == MODE_ROWSPLIT && P.capb > 0;
+        int pend = -1;  // B staging: tile index whose CSR slice is in flight
         for (int c = blockIdx.x; c < P.num_ranges; c += gridDim.x) {
             long long rs, zs, re, ze;
             if (MODE == MODE_ROWSPLIT) {
@@ -282,33 +353,40 @@ k_tile(const TileParams P) {
                 const bool last = (nr == re && nz == ze);
                 int b;
                 acquire(b);
+                uint64_t* csr_bar = bstage ? &landed[b] : &full[b];
                 if (lane == 0) {
                     uint32_t tx = 0;
                     TileInfo inf;
+                    inf.blo = 0;
                     inf.rs = (int)cr; inf.zs = (int)cz; inf.re = (int)nr; inf.ze = (int)nz;
                     inf.range = c;
                     bool staged;
                     fence_proxy_async_smem();
                     if (MODE == MODE_ROWSPLIT) {
                         staged = (nz - cz) + 8 <= capz;
-                        inf.ebase = te_stage(E_of(b), P.ro, cr, nr + 1, (long long)m + 1, &full[b], pol, &tx);
+                        inf.ebase = te_stage(E_of(b), P.ro, cr, nr + 1, (long long)m + 1, csr_bar, pol, &tx);
                     } else {
                         staged = true;
                         const long long e1 = min(nr + 1, (long long)m);  // row ends of rows cr..min(nr, m-1)
                         inf.ebase = te_stage(E_of(b), P.ro, cr + 1, e1 + 1, (long long)m + 1, &full[b], pol, &tx);
                     }
                     if (staged) {
-                        inf.zbase = te_stage(COL_of(b), P.col, cz, nz, P.nnz, &full[b], pol, &tx);
-                        te_stage(VAL_of(b), P.val, cz, nz, P.nnz, &full[b], pol, &tx);
+                        inf.zbase = te_stage(COL_of(b), P.col, cz, nz, P.nnz, csr_bar, pol, &tx);
+                        te_stage(VAL_of(b), P.val, cz, nz, P.nnz, csr_bar, pol, &tx);
                     } else {
                         inf.zbase = 0;
                     }
                     inf.flags = (first ? 1 : 0) | (last ? 2 : 0) | (staged ? 4 : 0);
                     *INFO_of(b) = inf;
-                    mbar_arrive_expect_tx(&full[b], tx);
+                    mbar_arrive_expect_tx(csr_bar, tx);
                 }
                 __syncwarp();
-                if (MODE == MODE_ROWSPLIT && P.pf_bytes && i >= 1) prefetch_tile_b((i - 1) % NS, i - 1);
+                if (bstage) {
+                    if (pend >= 0) finish_tile(pend % NS, pend);  // overlaps this tile's CSR load
+                    pend = i;
+                } else if (MODE == MODE_ROWSPLIT && P.pf_bytes && i >= 1) {
+                    prefetch_tile_b((i - 1) % NS, i - 1);
+                }
                 ++i;
                 first = false;
                 if (last) break;
@@ -316,6 +394,7 @@ k_tile(const TileParams P) {
                 cz = nz;
             }
         }
+        if (pend >= 0) finish_tile(pend % NS, pend);
         int b;
         acquire(b);
         if (lane == 0) {
@@ -346,6 +425,9 @@ k_tile(const TileParams P) {
         Blv[v] = opaque_ptr(static_cast<const char*>(P.B) +
                             (colok[v] ? (size_t)(gl * VEC + v * G * VEC) * sizeof(T) : (size_t)0));
     const char* Bl = Blv[0];
+    uint32_t boff[NV];  // byte offset of this lane's column block inside a B row (staged B span)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) boff[v] = colok[v] ? (uint32_t)((gl * VEC + v * G * VEC) * sizeof(T)) : 0u;
     T* Cl = static_cast<T*>(P.C) + gl * VEC;
     const unsigned ldb_bytes = P.ldb_bytes;
     const uint64_t bpol = B_L2_HINT ? policy_evict_last() : 0;
@@ -393,17 +475,26 @@ k_tile(const TileParams P) {
             const int rows = inf.re - inf.rs;
             const int NG = TE_CWARPS * S;
             const int gid = warp * S + slot;
-            const int rounds = (rows + NG - 1) / NG;
-            for (int t = 0; t < rounds; ++t) {
-                const int lr = t * NG + gid;
-                const bool active = lr < rows;
-                const int s = active ? E[inf.rs + lr - inf.ebase] : 0;
-                const int e = active ? E[inf.rs + lr + 1 - inf.ebase] : 0;
-                const int len = e - s;
-                const int maxlen = __reduce_max_sync(FULL, len);
-                Acc<T, SR, VEC, NV> accs[NA];  // NA interleaved partial sums: short FMA dependency chains
+            // one row's entries [s, s + len) into accs; every group of the warp runs the same trip count
+            // (B rows gathered from shared memory when the tile's B span is staged, else from global)
+            const bool bsm = inf.flags & 16;
+            const uint32_t bsb = smem_u32(BS_of(b)) - (uint32_t)inf.blo * ldb_bytes;
+            auto sgather = [&](unsigned (&o)[NV][VEC], int c, bool ok) {
 #pragma unroll
-                for (int k = 0; k < NA; ++k) accs[k].reset();
+                for (int v = 0; v < NV; ++v) lds_vpred<VEC>(o[v], bsb + (uint32_t)c * ldb_bytes + boff[v], ok);
+            };
+            auto sgather_full = [&](unsigned (&o)[NV][VEC], int c) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) lds_vec<VEC>(o[v], bsb + (uint32_t)c * ldb_bytes + boff[v]);
+            };
+            auto GF = [&](const bool kS, unsigned (&o)[NV][VEC], int c) {
+                if (kS) sgather_full(o, c); else gather_full(o, c);
+            };
+            auto GP = [&](const bool kS, unsigned (&o)[NV][VEC], int c, bool ok) {
+                if (kS) sgather(o, c, ok); else gather(o, c, ok);
+            };
+            auto row_pass = [&](const bool kS, const int s, const int len, Acc<T, SR, VEC, NV>(&accs)[NA]) {
+                const int maxlen = __reduce_max_sync(FULL, len);
                 if (staged) {
                     const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(s - inf.zbase);
                     const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(s - inf.zbase);
@@ -421,7 +512,7 @@ k_tile(const TileParams P) {
                                 av[u] = __shfl_sync(FULL, x, U + u, G);
                             }
 #pragma unroll
-                            for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+                            for (int u = 0; u < U; ++u) GF(kS, bv[u], (int)cu[u]);
 #pragma unroll
                             for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                             continue;
@@ -436,7 +527,7 @@ k_tile(const TileParams P) {
                                 av[u] = a4.x; av[u + 1] = a4.y; av[u + 2] = a4.z; av[u + 3] = a4.w;
                             }
 #pragma unroll
-                            for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+                            for (int u = 0; u < U; ++u) GF(kS, bv[u], (int)cu[u]);
 #pragma unroll
                             for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                             continue;
@@ -448,7 +539,7 @@ k_tile(const TileParams P) {
                                 av[u] = lds_u32(vs + 4u * (p0 + u));
                             }
 #pragma unroll
-                            for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
+                            for (int u = 0; u < U; ++u) GF(kS, bv[u], (int)cu[u]);
 #pragma unroll
                             for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                             continue;
@@ -459,7 +550,7 @@ k_tile(const TileParams P) {
                             av[u] = lds_pred(vs + 4u * (p0 + u), u < rem);
                         }
 #pragma unroll
-                        for (int u = 0; u < U; ++u) gather(bv[u], (int)cu[u], u < rem);
+                        for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], u < rem);
 #pragma unroll
                         for (int u = 0; u < U; ++u)
                             if (u < rem) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
@@ -477,15 +568,160 @@ k_tile(const TileParams P) {
                             av[u] = ldg_stream_pred(vg + p0 + u, u < rem);
                         }
 #pragma unroll
-                        for (int u = 0; u < U; ++u) gather(bv[u], (int)cu[u], u < rem);
+                        for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], u < rem);
 #pragma unroll
                         for (int u = 0; u < U; ++u)
                             if (u < rem) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
                     }
                 }
+            };
+            bool tile_done = false;
+            if constexpr (PAIR) {
+                auto pair_body = [&](const bool kS) {
+                    // Row pairs (B200 extension of §4.1): a group owns rows (2i, 2i+1) =
+                    // (L, Q).  Q's entry j is matched with L's entry j + delta (delta = #{L cols < Q's first
+                    // col}); when the columns agree, the B row gathered for L's entry also feeds Q, so a
+                    // banded pair gathers 17 B rows instead of 32.  Q's unmatched entries are gathered
+                    // afterwards.  Every entry is used exactly once whatever the column order, so the
+                    // result is C = AB for any CSR (sorted columns only make the matching effective).
+                    const int pairs = (rows + 1) >> 1;
+                    const int prounds = (pairs + NG - 1) / NG;
+                    const uint32_t colz = smem_u32(COL) - 4u * (uint32_t)inf.zbase;  // + 4p: column of nonzero p
+                    const uint32_t valz = smem_u32(VAL) - 4u * (uint32_t)inf.zbase;
+                    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (slot * G));
+                    for (int t = 0; t < prounds; ++t) {
+                        const int lr = 2 * (t * NG + gid);
+                        const bool actL = lr < rows;
+                        const bool actQ = lr + 1 < rows;
+                        const int sL = actL ? E[inf.rs + lr - inf.ebase] : 0;
+                        const int eL = actL ? E[inf.rs + lr + 1 - inf.ebase] : 0;
+                        const int eQ = actQ ? E[inf.rs + lr + 2 - inf.ebase] : eL;
+                        const int lenL = eL - sL, lenQ = eQ - eL;
+                        if (!__all_sync(FULL, lenL <= 32 && lenQ <= 32)) {
+                            // a long row in the warp: the two rows one after the other (plain row split)
+#pragma unroll 1
+                            for (int h = 0; h < 2; ++h) {
+                                Acc<T, SR, VEC, NV> accs[NA];
 #pragma unroll
-                for (int k = 1; k < NA; ++k) accs[0].fold(accs[k]);
-                store_row(inf.rs + lr, accs[0], active);
+                                for (int k = 0; k < NA; ++k) accs[k].reset();
+                                row_pass(kS, h ? eL : sL, h ? lenQ : lenL, accs);
+#pragma unroll
+                                for (int k = 1; k < NA; ++k) accs[0].fold(accs[k]);
+                                store_row(inf.rs + lr + h, accs[0], h ? actQ : actL);
+                            }
+                            continue;
+                        }
+                        const int maxL = __reduce_max_sync(FULL, lenL);
+                        const int q0 = (lenQ > 0) ? (int)lds_u32(colz + 4u * (uint32_t)eL) : 0x7fffffff;
+                        int delta = 0;
+                        for (int k0 = 0; k0 < maxL; k0 += G) {
+                            const int i = k0 + gl;
+                            const bool in = i < lenL;
+                            const bool lt = in && (int)lds_pred(colz + 4u * (uint32_t)(sL + i), in) < q0;
+                            delta += __popc(__ballot_sync(FULL, lt) & gmask);
+                        }
+#ifndef RSP_NA
+#define RSP_NA 1  // interleaved partial sums for the pair's first row (its second row has one)
+#endif
+                        constexpr int PNA = RSP_NA;
+                        Acc<T, SR, VEC, NV> accL[PNA], accQ;
+#pragma unroll
+                        for (int k = 0; k < PNA; ++k) accL[k].reset();
+                        accQ.reset();
+                        uint32_t used = 0;  // bit j: Q's entry j was consumed with its partner in L
+                        // L's batches are visited in an order rotated by the group's slot: the groups of a
+                        // warp then read (col, val) from different shared-memory banks (pairs of equal
+                        // length start on the same bank), so each LDS.128 is one wavefront
+                        const int nb = (maxL + U - 1) / U;
+                        for (int bi = 0; bi < nb; ++bi) {
+                            const int p0 = ((bi + slot) % nb) * U;
+                            const int rem = lenL - p0;
+                            unsigned bv[U][NV][VEC];
+                            unsigned cu[U], av[U], aq[U];
+                            bool qm[U];
+                            const uint32_t ca = colz + 4u * (uint32_t)(sL + p0);
+                            const uint32_t va = valz + 4u * (uint32_t)(sL + p0);
+                            if (U % 4 == 0 && __all_sync(FULL, rem >= U && (ca & 15u) == 0)) {
+#pragma unroll
+                                for (int u = 0; u < U; u += 4) {
+                                    const uint4 c4 = lds_u128(ca + 4u * u);
+                                    const uint4 a4 = lds_u128(va + 4u * u);
+                                    cu[u] = c4.x; cu[u + 1] = c4.y; cu[u + 2] = c4.z; cu[u + 3] = c4.w;
+                                    av[u] = a4.x; av[u + 1] = a4.y; av[u + 2] = a4.z; av[u + 3] = a4.w;
+                                }
+                            } else {
+#pragma unroll
+                                for (int u = 0; u < U; ++u) {
+                                    cu[u] = lds_pred(ca + 4u * u, u < rem);
+                                    av[u] = lds_pred(va + 4u * u, u < rem);
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                const bool in = u < rem;
+                                const int j = p0 + u - delta;
+                                const bool qok = in && (unsigned)j < (unsigned)lenQ;
+                                const unsigned cq = lds_pred(colz + 4u * (uint32_t)(eL + j), qok);
+                                aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j), qok);
+                                qm[u] = qok && cq == cu[u];
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], u < rem);
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                if (u < rem) accL[u % PNA].mac(from_bits<T>(av[u]), bv[u]);
+                                if (qm[u]) {
+                                    accQ.mac(from_bits<T>(aq[u]), bv[u]);
+                                    used |= 1u << (p0 + u - delta);
+                                }
+                            }
+                        }
+                        uint32_t todo = (lenQ >= 32 ? 0xffffffffu : ((1u << lenQ) - 1u)) & ~used;
+                        const int maxc = __reduce_max_sync(FULL, __popc(todo));
+                        for (int c0 = 0; c0 < maxc; c0 += U) {
+                            unsigned bv[U][NV][VEC];
+                            unsigned aq[U];
+                            bool ok[U];
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                ok[u] = todo != 0u;
+                                const int j = ok[u] ? __ffs((int)todo) - 1 : 0;
+                                todo &= todo - 1u;
+                                const unsigned cq = lds_pred(colz + 4u * (uint32_t)(eL + j), ok[u]);
+                                aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j), ok[u]);
+                                if (c0 + u < maxc) GP(kS, bv[u], (int)cq, ok[u]);
+                            }
+#pragma unroll
+                            for (int u = 0; u < U; ++u)
+                                if (ok[u]) accQ.mac(from_bits<T>(aq[u]), bv[u]);
+                        }
+#pragma unroll
+                        for (int k = 1; k < PNA; ++k) accL[0].fold(accL[k]);
+                        store_row(inf.rs + lr, accL[0], actL);
+                        store_row(inf.rs + lr + 1, accQ, actQ);
+                    }
+                };
+                if (staged) {
+                    if (bsm) pair_body(true); else pair_body(false);
+                    tile_done = true;
+                }
+            }
+            if (!tile_done) {
+                const int rounds = (rows + NG - 1) / NG;
+                for (int t = 0; t < rounds; ++t) {
+                    const int lr = t * NG + gid;
+                    const bool active = lr < rows;
+                    const int s = active ? E[inf.rs + lr - inf.ebase] : 0;
+                    const int e = active ? E[inf.rs + lr + 1 - inf.ebase] : 0;
+                    Acc<T, SR, VEC, NV> accs[NA];  // NA interleaved partial sums: short FMA dependency chains
+#pragma unroll
+                    for (int k = 0; k < NA; ++k) accs[k].reset();
+                    if (bsm) row_pass(true, s, e - s, accs);
+                    else row_pass(false, s, e - s, accs);
+#pragma unroll
+                    for (int k = 1; k < NA; ++k) accs[0].fold(accs[k]);
+                    store_row(inf.rs + lr, accs[0], active);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[b]);
@@ -835,6 +1071,19 @@ k_tile(const TileParams P) {
             named_bar_sync(1, TE_CONSUMERS);
         }
     }
+}
+
+template <typename T, int SR, int MODE, int VEC, int G, int NV, int U>
+__global__ void __launch_bounds__(TE_THREADS, MODE == MODE_MERGE ? TE_MINB_MG : TE_MINB) k_tile(const TileParams P) {
+    tile_body<T, SR, MODE, VEC, G, NV, U, false>(P);
+}
+
+#ifndef RSP_MAXREG
+#define RSP_MAXREG 96  // 9 warps per CTA land 5/4 per SMSP: 2 CTAs per SM need <= 96 registers (64K per SMSP quarter)
+#endif
+template <typename T, int SR, int VEC, int G, int NV, int U>
+__global__ void __maxnreg__(RSP_MAXREG) k_tile_pair(const TileParams P) {
+    tile_body<T, SR, MODE_ROWSPLIT, VEC, G, NV, U, true>(P);
 }
 
 }  // namespace spmm

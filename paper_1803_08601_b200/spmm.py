@@ -31,6 +31,8 @@ SPMM_PLUS_TIMES, SPMM_MIN_PLUS = 0, 1
 SPMM_FLAG_VALIDATE = 1
 SPMM_POLICY_AUTO, SPMM_POLICY_PAPER = 0, 1
 SPMM_PARTITION_MERGE_PATH, SPMM_PARTITION_NONZERO_SPLIT = 0, 1
+SPMM_PAIRING_AUTO, SPMM_PAIRING_OFF, SPMM_PAIRING_ON = 0, 1, 2
+PAIRINGS = {"auto": SPMM_PAIRING_AUTO, "off": SPMM_PAIRING_OFF, "on": SPMM_PAIRING_ON}
 
 ALGOS = {"auto": SPMM_ALGO_AUTO, "rowsplit": SPMM_ALGO_ROWSPLIT, "merge": SPMM_ALGO_MERGE}
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
@@ -43,7 +45,7 @@ EXPORTED = ("spmm_csr_create", "spmm_csr_plan", "spmm_csr_plan_ex", "spmm_csr_ex
 
 class spmm_plan_opts(Structure):
     _fields_ = [("policy", c_int32), ("partition", c_int32), ("items_per_cta", c_int32),
-                ("reserved", c_int32 * 5)]
+                ("row_pairing", c_int32), ("reserved", c_int32 * 4)]
 
 
 class spmm_plan_info(Structure):
@@ -51,7 +53,7 @@ class spmm_plan_info(Structure):
                 ("semiring", c_int32), ("dtype", c_int32), ("policy", c_int32), ("partition", c_int32),
                 ("mean_row_length", c_double), ("max_row_length", c_int64), ("threshold", c_double),
                 ("num_ctas", c_int32), ("items_per_cta", c_int32), ("launches_per_execute", c_int32),
-                ("reserved0", c_int32), ("workspace_bytes", c_size_t)]
+                ("row_pairing", c_int32), ("workspace_bytes", c_size_t)]
 
 
 class SpmmError(RuntimeError):
@@ -136,8 +138,9 @@ def spmm_csr_plan(h, n, algo, semiring, threshold=0.0, stream=None):
     return st, ws.value, chosen.value
 
 
-def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None):
-    o = spmm_plan_opts(policy, partition, items_per_cta)
+def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None,
+                     row_pairing=0):
+    o = spmm_plan_opts(policy, partition, items_per_cta, row_pairing)
     ws = c_size_t(0)
     chosen = c_int32(0)
     st = load().spmm_csr_plan_ex(h, n, algo, semiring, threshold, ctypes.byref(o), stream, ctypes.byref(ws),
@@ -224,13 +227,14 @@ class CsrSpmm:
         self.chosen = None
 
     def plan(self, n: int, algo: str = "auto", semiring: str = "plus_times", threshold: float = 0.0,
-             policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None) -> str:
+             policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None,
+             row_pairing: str = "auto") -> str:
         import torch
         st, ws, chosen = spmm_csr_plan_ex(self._h, n, ALGOS[algo], SEMIRINGS[semiring], threshold,
                                           {"auto": SPMM_POLICY_AUTO, "paper": SPMM_POLICY_PAPER}[policy],
                                           {"merge_path": SPMM_PARTITION_MERGE_PATH,
                                            "nonzero_split": SPMM_PARTITION_NONZERO_SPLIT}[partition],
-                                          items_per_cta, _stream_ptr(stream))
+                                          items_per_cta, _stream_ptr(stream), PAIRINGS[row_pairing])
         _check(st, self._h)
         self.n = n
         self.workspace = torch.empty(max(ws, 16), dtype=torch.uint8, device=self.row_offsets.device)
@@ -241,7 +245,7 @@ class CsrSpmm:
     def info(self) -> dict:
         st, inf = spmm_csr_get_plan_info(self._h)
         _check(st, self._h)
-        return {f: getattr(inf, f) for f, _ in spmm_plan_info._fields_ if f != "reserved0"}
+        return {f: getattr(inf, f) for f, _ in spmm_plan_info._fields_}
 
     def execute(self, B, C=None, stream=None):
         import torch
