@@ -57,6 +57,9 @@ constexpr int kNumSMs = 148;
 #ifndef MG_FOLD
 #define MG_FOLD 0  // merge with lane-folded workers for n <= 16 (experimental; slower on B200 so far)
 #endif
+#ifndef RS_GDIV
+#define RS_GDIV 2  // row split, 16..32 vector lanes per row: split the row over lanes/RS_GDIV lanes
+#endif
 #ifndef TE_CARVE
 #define TE_CARVE 1  // request the minimal shared-memory carveout (maximal L1) for the resident CTAs
 #endif
@@ -228,7 +231,7 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
         // column blocks each (n = 64: 8 lanes x 2 float4) -- more rows per warp, fewer broadcast loads
         const int G0 = std::min(32, pow2ceil(lanes));
         if (lanes <= 32 && G0 >= 16) {
-            c.G = G0 / 2;
+            c.G = G0 / RS_GDIV;
             c.NV = (lanes + c.G - 1) / c.G;
         } else {
             c.G = G0;
@@ -335,6 +338,7 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
     case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kRowsplitU>(P, st); break;
     switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
         RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 8, 2) RS_CASE(4, 16, 2)
+        RS_CASE(4, 4, 4) RS_CASE(4, 8, 4)
         RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 8, 2) RS_CASE(2, 16, 2)
         RS_CASE(2, 32, 2)
         RS_CASE(1, 1, 1) RS_CASE(1, 2, 1) RS_CASE(1, 4, 1) RS_CASE(1, 8, 1) RS_CASE(1, 8, 2) RS_CASE(1, 16, 2)

@@ -411,23 +411,32 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
 #ifndef MG_NA
 #define MG_NA 4
 #endif
-    constexpr int NA = (MODE == MODE_MERGE) ? ((VEC * NV <= 2) ? MG_NA : 2) : 2;
+#ifndef RS_NA
+#define RS_NA 2
+#endif
+    constexpr int NA = (MODE == MODE_MERGE) ? ((VEC * NV <= 2) ? MG_NA : 2) : RS_NA;
     const int slot = lane / G;
     const int gl = lane - slot * G;
     bool colok[NV];
+    // column offset of this lane's v-th vector block; the blocks are rotated by the group's slot so
+    // that groups reading different B rows at the same time cover different shared-memory banks
+    // when a group's block is narrower than 128 B (G * VEC < 32)
+    int cofs[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) colok[v] = (gl * VEC + v * G * VEC) < n;
+    for (int v = 0; v < NV; ++v) cofs[v] = gl * VEC + ((v + slot) % NV) * G * VEC;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) colok[v] = cofs[v] < n;
     // per-lane B base of each column block; lanes past n read column 0 of the same row instead
     // (valid memory, never stored), so the gathers need no column predicate or branch
     const char* Blv[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
         Blv[v] = opaque_ptr(static_cast<const char*>(P.B) +
-                            (colok[v] ? (size_t)(gl * VEC + v * G * VEC) * sizeof(T) : (size_t)0));
+                            (colok[v] ? (size_t)cofs[v] * sizeof(T) : (size_t)0));
     const char* Bl = Blv[0];
     uint32_t boff[NV];  // byte offset of this lane's column block inside a B row (staged B span)
 #pragma unroll
-    for (int v = 0; v < NV; ++v) boff[v] = colok[v] ? (uint32_t)((gl * VEC + v * G * VEC) * sizeof(T)) : 0u;
+    for (int v = 0; v < NV; ++v) boff[v] = colok[v] ? (uint32_t)(cofs[v] * sizeof(T)) : 0u;
     T* Cl = static_cast<T*>(P.C) + gl * VEC;
     const unsigned ldb_bytes = P.ldb_bytes;
     const uint64_t bpol = B_L2_HINT ? policy_evict_last() : 0;
@@ -448,7 +457,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 unsigned o[VEC];
 #pragma unroll
                 for (int x = 0; x < VEC; ++x) o[x] = to_bits<T>(acc.v[v][x]);
-                st_vec<VEC>(crow + v * G * VEC, o);
+                st_vec<VEC>(crow + (cofs[v] - gl * VEC), o);
             }
         }
     };
@@ -701,8 +710,8 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                         store_row(inf.rs + lr + 1, accQ, actQ);
                     }
                 };
-                if (staged) {
-                    if (bsm) pair_body(true); else pair_body(false);
+                if (staged && bsm) {  // pairs only from a staged B span (short latencies); else plain rows
+                    pair_body(true);
                     tile_done = true;
                 }
             }
@@ -756,7 +765,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 for (int v = 0; v < NV; ++v)
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) {
-                        const int cc = gl * VEC + v * G * VEC + x;
+                        const int cc = cofs[v] + x;
                         acc.v[v][x] = (cc < n) ? Cw[NWK * n + cc] : R::id();
                     }
                 dirty = true;
@@ -1013,7 +1022,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                     for (int v = 0; v < NV; ++v)
 #pragma unroll
                         for (int x = 0; x < VEC; ++x) {
-                            const int cc = gl * VEC + v * G * VEC + x;
+                            const int cc = cofs[v] + x;
                             if (colok[v] && cc < n) slots[wid * n + cc] = acc.v[v][x];
                         }
                 }
