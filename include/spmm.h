@@ -100,6 +100,11 @@ typedef struct {
     int32_t launches_per_execute;  /* kernels one execute() enqueues (row split 1, merge 3) */
     int32_t row_pairing;     /* 1 if the row-split kernel runs on row pairs (see spmm_plan_opts) */
     size_t workspace_bytes;
+    int32_t b_staging;       /* 1 if the row-split kernel stages compact B row spans in shared memory
+                                (TMA); measured at plan time, applied per tile at execute when B and
+                                ldb allow 16-byte aligned rows                          */
+    int32_t rows_per_tile;   /* row split: rows per tile                                               */
+    double bspan_compact;    /* fraction of nonzeros in tiles whose B span is compact (-1: not measured) */
 } spmm_plan_info;
 
 /*

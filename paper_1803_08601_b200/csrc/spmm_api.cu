@@ -594,6 +594,9 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         int R = 1;
         while (R * 2 <= 4096 && R * 2 * dd <= (double)RS_TILE_NNZ) R *= 2;
         R = std::max(16, std::min(R, 1024));
+#ifdef RS_R_FORCE
+        R = RS_R_FORCE;
+#endif
         auto capz_for = [&](int rows) {
             long long z = (long long)std::ceil(RS_ZF / 10.0 * rows * dd);
             z = std::max<long long>(1024, std::min<long long>(z, 8192));
@@ -686,6 +689,9 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
     out->items_per_cta = h->chosen == SPMM_ALGO_MERGE ? h->items : 0;
     out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : 1);
     out->row_pairing = (h->chosen == SPMM_ALGO_ROWSPLIT && h->pairing) ? 1 : 0;
+    out->b_staging = (h->chosen == SPMM_ALGO_ROWSPLIT && h->capb > 0) ? 1 : 0;
+    out->rows_per_tile = h->chosen == SPMM_ALGO_ROWSPLIT ? h->rows_per_tile : 0;
+    out->bspan_compact = h->bspan_compact;
     out->workspace_bytes = h->ws_bytes;
     return SPMM_OK;
 }

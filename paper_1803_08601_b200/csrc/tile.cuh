@@ -586,18 +586,20 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             };
             bool tile_done = false;
             if constexpr (PAIR) {
-                auto pair_body = [&](const bool kS) {
-                    // Row pairs (B200 extension of §4.1): a group owns rows (2i, 2i+1) =
-                    // (L, Q).  Q's entry j is matched with L's entry j + delta (delta = #{L cols < Q's first
-                    // col}); when the columns agree, the B row gathered for L's entry also feeds Q, so a
-                    // banded pair gathers 17 B rows instead of 32.  Q's unmatched entries are gathered
-                    // afterwards.  Every entry is used exactly once whatever the column order, so the
-                    // result is C = AB for any CSR (sorted columns only make the matching effective).
+                auto pair_body = [&]() {
+                    // Row pairs (B200 extension of §4.1), only for tiles whose B span is
+                    // staged in shared memory: a group owns rows (2i, 2i+1) = (L, Q).  Q's entry j is
+                    // matched with L's entry j + delta (delta = #{L cols < Q's first col}) when the two
+                    // columns are equal; the B row read for L's entry then also feeds Q, so a banded pair
+                    // reads 17 B rows into registers instead of 32.  Q's unmatched entries are read
+                    // afterwards.  Every stored entry is used exactly once whatever the column order, so
+                    // the result is C = AB for any CSR (sorted columns only make the matching effective).
+                    constexpr bool kS = true;
                     const int pairs = (rows + 1) >> 1;
                     const int prounds = (pairs + NG - 1) / NG;
                     const uint32_t colz = smem_u32(COL) - 4u * (uint32_t)inf.zbase;  // + 4p: column of nonzero p
                     const uint32_t valz = smem_u32(VAL) - 4u * (uint32_t)inf.zbase;
-                    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (slot * G));
+                    const unsigned gbits = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
                     for (int t = 0; t < prounds; ++t) {
                         const int lr = 2 * (t * NG + gid);
                         const bool actL = lr < rows;
@@ -621,33 +623,37 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                             continue;
                         }
                         const int maxL = __reduce_max_sync(FULL, lenL);
+                        const int maxQ = __reduce_max_sync(FULL, lenQ);
+                        // delta and the match mask, the group's lanes in parallel
                         const int q0 = (lenQ > 0) ? (int)lds_u32(colz + 4u * (uint32_t)eL) : 0x7fffffff;
                         int delta = 0;
                         for (int k0 = 0; k0 < maxL; k0 += G) {
                             const int i = k0 + gl;
                             const bool in = i < lenL;
                             const bool lt = in && (int)lds_pred(colz + 4u * (uint32_t)(sL + i), in) < q0;
-                            delta += __popc(__ballot_sync(FULL, lt) & gmask);
+                            delta += __popc((__ballot_sync(FULL, lt) >> (slot * G)) & gbits);
                         }
-#ifndef RSP_NA
-#define RSP_NA 1  // interleaved partial sums for the pair's first row (its second row has one)
-#endif
-                        constexpr int PNA = RSP_NA;
-                        Acc<T, SR, VEC, NV> accL[PNA], accQ;
-#pragma unroll
-                        for (int k = 0; k < PNA; ++k) accL[k].reset();
+                        uint32_t mask = 0;  // bit j: Q's entry j is paired with L's entry j + delta
+                        for (int k0 = 0; k0 < maxQ; k0 += G) {
+                            const int j = k0 + gl;
+                            const bool in = j < lenQ && j + delta < lenL;
+                            const unsigned a = lds_pred(colz + 4u * (uint32_t)(eL + j), in);
+                            const unsigned c = lds_pred(colz + 4u * (uint32_t)(sL + j + delta), in);
+                            const unsigned bits = (__ballot_sync(FULL, in && a == c) >> (slot * G)) & gbits;
+                            mask |= bits << k0;
+                        }
+                        Acc<T, SR, VEC, NV> accL, accQ;
+                        accL.reset();
                         accQ.reset();
-                        uint32_t used = 0;  // bit j: Q's entry j was consumed with its partner in L
-                        // L's batches are visited in an order rotated by the group's slot: the groups of a
-                        // warp then read (col, val) from different shared-memory banks (pairs of equal
-                        // length start on the same bank), so each LDS.128 is one wavefront
+                        // L's batches in an order rotated by the group's slot (bank spread)
                         const int nb = (maxL + U - 1) / U;
+                        int bb = slot % nb;
                         for (int bi = 0; bi < nb; ++bi) {
-                            const int p0 = ((bi + slot) % nb) * U;
+                            const int p0 = bb * U;
+                            bb = (bb + 1 == nb) ? 0 : bb + 1;
                             const int rem = lenL - p0;
                             unsigned bv[U][NV][VEC];
                             unsigned cu[U], av[U], aq[U];
-                            bool qm[U];
                             const uint32_t ca = colz + 4u * (uint32_t)(sL + p0);
                             const uint32_t va = valz + 4u * (uint32_t)(sL + p0);
                             if (U % 4 == 0 && __all_sync(FULL, rem >= U && (ca & 15u) == 0)) {
@@ -665,27 +671,22 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                                     av[u] = lds_pred(va + 4u * u, u < rem);
                                 }
                             }
+                            // mask bits of Q entries p0 - delta .. p0 - delta + U - 1
+                            const int j0 = p0 - delta;
+                            const uint32_t mw = (j0 >= 0) ? (j0 < 32 ? (mask >> j0) : 0u) : (mask << (-j0 < 32 ? -j0 : 31)) & (-j0 < 32 ? 0xffffffffu : 0u);
 #pragma unroll
-                            for (int u = 0; u < U; ++u) {
-                                const bool in = u < rem;
-                                const int j = p0 + u - delta;
-                                const bool qok = in && (unsigned)j < (unsigned)lenQ;
-                                const unsigned cq = lds_pred(colz + 4u * (uint32_t)(eL + j), qok);
-                                aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j), qok);
-                                qm[u] = qok && cq == cu[u];
-                            }
+                            for (int u = 0; u < U; ++u)
+                                aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j0 + u), (mw >> u) & 1u);
 #pragma unroll
                             for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], u < rem);
 #pragma unroll
                             for (int u = 0; u < U; ++u) {
-                                if (u < rem) accL[u % PNA].mac(from_bits<T>(av[u]), bv[u]);
-                                if (qm[u]) {
-                                    accQ.mac(from_bits<T>(aq[u]), bv[u]);
-                                    used |= 1u << (p0 + u - delta);
-                                }
+                                if (u < rem) accL.mac(from_bits<T>(av[u]), bv[u]);
+                                if ((mw >> u) & 1u) accQ.mac(from_bits<T>(aq[u]), bv[u]);
                             }
                         }
-                        uint32_t todo = (lenQ >= 32 ? 0xffffffffu : ((1u << lenQ) - 1u)) & ~used;
+                        // Q's entries without a partner
+                        uint32_t todo = (lenQ >= 32 ? 0xffffffffu : ((1u << lenQ) - 1u)) & ~mask;
                         const int maxc = __reduce_max_sync(FULL, __popc(todo));
                         for (int c0 = 0; c0 < maxc; c0 += U) {
                             unsigned bv[U][NV][VEC];
@@ -704,14 +705,12 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                             for (int u = 0; u < U; ++u)
                                 if (ok[u]) accQ.mac(from_bits<T>(aq[u]), bv[u]);
                         }
-#pragma unroll
-                        for (int k = 1; k < PNA; ++k) accL[0].fold(accL[k]);
-                        store_row(inf.rs + lr, accL[0], actL);
+                        store_row(inf.rs + lr, accL, actL);
                         store_row(inf.rs + lr + 1, accQ, actQ);
                     }
                 };
                 if (staged && bsm) {  // pairs only from a staged B span (short latencies); else plain rows
-                    pair_body(true);
+                    pair_body();
                     tile_done = true;
                 }
             }

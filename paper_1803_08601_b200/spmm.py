@@ -53,7 +53,8 @@ class spmm_plan_info(Structure):
                 ("semiring", c_int32), ("dtype", c_int32), ("policy", c_int32), ("partition", c_int32),
                 ("mean_row_length", c_double), ("max_row_length", c_int64), ("threshold", c_double),
                 ("num_ctas", c_int32), ("items_per_cta", c_int32), ("launches_per_execute", c_int32),
-                ("row_pairing", c_int32), ("workspace_bytes", c_size_t)]
+                ("row_pairing", c_int32), ("workspace_bytes", c_size_t), ("b_staging", c_int32),
+                ("rows_per_tile", c_int32), ("bspan_compact", c_double)]
 
 
 class SpmmError(RuntimeError):

@@ -409,3 +409,44 @@ def test_row_pairing_bit_identical_in_exact_semirings_and_auto_choice():
         op.plan(64, "rowsplit", row_pairing="off")
         assert op.info()["row_pairing"] == 0
         op.close()
+
+
+# ------------------------------------------------------------------------------------------------
+# B staging of the row-split kernel (compact B row spans copied to shared memory by TMA)
+# ------------------------------------------------------------------------------------------------
+def _banded_with_far_entries(m: int, every: int, seed: int = 3):
+    """Band of 9 plus, in every `every`-th row, one far column: tiles holding such a row have a
+    scattered B span and keep the global gathers; the others are staged."""
+    cols, ro = [], [0]
+    for i in range(m):
+        row = sorted({(i + o) % m for o in range(-4, 5)} | ({(i * 7919 + seed * 104729) % m} if i % every == 0 else set()))
+        cols += row
+        ro.append(len(cols))
+    return synth.CsrPattern(m, m, torch.tensor(ro, dtype=torch.int32), torch.tensor(cols, dtype=torch.int32),
+                            f"band_far{every}")
+
+
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("n", [1, 3, 8, 16, 31, 64, 100, 128])
+@pytest.mark.parametrize("case", ["aligned", "ldb_pad", "misaligned", "mixed_tiles"])
+def test_b_staging_parity(kind, n, case):
+    p = _banded_with_far_entries(4099, 700) if case == "mixed_tiles" else synth.banded(4099, lo=5, hi=9)
+    ldb = n + 4 if case == "ldb_pad" else None
+    off = 1 if case == "misaligned" else 0
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, ldb=ldb, b_offset=off)
+    chosen, info = run_gpu(p, kind, n, "rowsplit", ro, ci, vd, Bd, Cd)
+    assert chosen == "rowsplit"
+    assert info["b_staging"] == 1 and info["bspan_compact"] >= 0.5
+    check(p, kind, n, val, Bh, Cd)
+
+
+def test_b_staging_plan_decision():
+    """Compact (banded) spans are staged; uniform-random columns are not."""
+    for pat, want in ((synth.banded(1 << 14), 1), (synth.uniform_rows(1 << 14, 1 << 14, 16, 5), 0)):
+        vd = synth.values(pat.nnz, 1, "f32_plus_times").to(DEV)
+        op = S.CsrSpmm(pat.row_offsets.to(DEV), pat.col_indices.to(DEV), vd, pat.k)
+        assert op.plan(64, "rowsplit") == "rowsplit"
+        inf = op.info()
+        assert inf["b_staging"] == want, inf
+        assert (inf["bspan_compact"] > 0.9) == bool(want)
+        op.close()
