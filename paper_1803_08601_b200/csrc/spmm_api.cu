@@ -278,6 +278,12 @@ cudaError_t launch_tile(TileParams P, cudaStream_t st) {
     }
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+#if TE_CARVE
+    // the carveout preference is sticky per kernel: size the occupancy query with the full shared
+    // memory array, not with the carveout an earlier (smaller) launch of this kernel asked for
+    e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+#endif
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, TE_THREADS, smem);
     if (e != cudaSuccess) return e;
