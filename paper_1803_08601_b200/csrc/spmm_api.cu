@@ -88,9 +88,6 @@ constexpr int kPairU = RSP_U;
 #ifndef RS_BSTAGE
 #define RS_BSTAGE 1  // row split: stage compact B row spans into shared memory with TMA (plan-time measured)
 #endif
-#ifndef RS_HALO_F
-#define RS_HALO_F 2.0
-#endif
 #ifndef RS_BSTAGE_MIN
 #define RS_BSTAGE_MIN 0.5  // stage B when at least this fraction of the nonzeros lies in compact tiles
 #endif
@@ -165,13 +162,13 @@ __global__ void k_pair_share(const int* __restrict__ ro, const int* __restrict__
 
 // B-span compactness for the row-split kernel's B staging: warp per row tile of R rows; a tile is
 // compact when its column span [lo, hi] holds at most 2 B rows per nonzero and fits capb bytes at
-// row_bytes per row.  out[0] += nonzeros of compact tiles.
+// row_bytes per row.  out[0] += nonzeros of compact tiles; out[1] = max bytes of a compact span.
 __global__ void k_tile_span(const int* __restrict__ ro, const int* __restrict__ col, long long m, int R,
                             long long row_bytes, long long capb, unsigned long long* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const long long tiles = (m + R - 1) / R;
     const long long nw = (long long)gridDim.x * (blockDim.x / 32);
-    unsigned long long acc = 0;
+    unsigned long long acc = 0, mx = 0;
     for (long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32; t < tiles; t += nw) {
         const long long rs = t * R, re = min(m, rs + R);
         const int zs = ro[rs], ze = ro[re];
@@ -184,9 +181,15 @@ __global__ void k_tile_span(const int* __restrict__ ro, const int* __restrict__ 
         lo = __reduce_min_sync(FULL, lo);
         hi = __reduce_max_sync(FULL, hi);
         const long long cnt = ze - zs, span = (long long)hi - lo + 1;
-        if (cnt > 0 && span <= 2 * cnt && span * row_bytes <= capb) acc += (unsigned long long)cnt;
+        if (cnt > 0 && span <= 2 * cnt && span * row_bytes <= capb) {
+            acc += (unsigned long long)cnt;
+            mx = max(mx, (unsigned long long)(span * row_bytes));
+        }
     }
-    if (lane == 0 && acc) atomicAdd(out, acc);
+    if (lane == 0 && acc) {
+        atomicAdd(out, acc);
+        atomicMax(out + 1, mx);
+    }
 }
 
 // flags: bit0 ro[0] != 0, bit1 decreasing offsets, bit2 ro[m] != nnz, bit3 column out of range
@@ -612,39 +615,37 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         h->capz = capz_for(R);
         h->capb = 0;
         h->bspan_compact = -1.0;
-        if (RS_BSTAGE && h->nnz > 0) {
-            // B staging: smaller tiles whose B row span (R_b rows + the band around them)
-            // fits a per-stage shared-memory slot next to the CSR slice, 3 stages x 2 CTAs per SM
-            const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
-            const long long row_bytes = (long long)((n * elem + 15) & ~(size_t)15);
-            const int halo = std::max(16, (int)std::ceil(RS_HALO_F * dd));  // B rows beyond R the span may need
-            int Rb = R;
-            long long capb = 0;
-            while (true) {
-                capb = ((long long)(Rb + halo) * row_bytes + 15) & ~15LL;
-                const long long stage = (long long)te_buf_bytes(Rb + 8, capz_for(Rb), (int)elem, (int)capb);
-                if (RS_STAGES * stage <= RS_BSTAGE_SMEM || Rb <= 16) break;
-                Rb /= 2;
-            }
-            if (RS_STAGES * (long long)te_buf_bytes(Rb + 8, capz_for(Rb), (int)elem, (int)capb) <= RS_BSTAGE_SMEM) {
-                cudaStream_t st = static_cast<cudaStream_t>(stream);
-                unsigned long long cnt = 0;
-                unsigned long long* dc = reinterpret_cast<unsigned long long*>(h->d_scratch + 4);
+        const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
+        if (RS_BSTAGE && h->nnz > 0 && (n * elem) % 16 == 0) {
+            // B staging: the largest tile height R_b <= R whose tiles' B row spans fit
+            // the shared memory left next to the CSR slice (3 stages x 2 CTAs per SM) for at least
+            // RS_BSTAGE_MIN of the nonzeros; the per-stage B slot is then sized to the largest
+            // compact span measured.  The B row pitch is assumed to be n (execute re-checks per tile).
+            const long long row_bytes = (long long)(n * elem);
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            unsigned long long* dc = reinterpret_cast<unsigned long long*>(h->d_scratch + 4);
+            for (int Rb = R; Rb >= 16; Rb /= 2) {
+                const long long csr = (long long)te_buf_bytes(Rb + 8, capz_for(Rb), (int)elem, 0);
+                const long long capb_try = ((RS_BSTAGE_SMEM / RS_STAGES - csr) / 16) * 16;
+                if (capb_try < 16 * row_bytes) continue;
+                unsigned long long cnt[2] = {0, 0};
                 cudaError_t e = cudaMemsetAsync(dc, 0, sizeof(cnt), st);
                 if (e == cudaSuccess) {
                     const long long tiles = (h->m + Rb - 1) / Rb;
                     const int grid = (int)std::min<long long>((tiles + WARPS_PER_CTA - 1) / WARPS_PER_CTA, 8LL * kNumSMs);
-                    k_tile_span<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, Rb, row_bytes, capb, dc);
+                    k_tile_span<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, Rb, row_bytes, capb_try, dc);
                     e = cudaGetLastError();
                 }
-                if (e == cudaSuccess) e = cudaMemcpyAsync(&cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, st);
                 if (e == cudaSuccess) e = cudaStreamSynchronize(st);
                 if (e != cudaSuccess) return cuda_fail(h, e, "plan: B span");
-                h->bspan_compact = (double)cnt / (double)h->nnz;
-                if (h->bspan_compact >= RS_BSTAGE_MIN) {
+                const double frac = (double)cnt[0] / (double)h->nnz;
+                h->bspan_compact = std::max(h->bspan_compact, frac);
+                if (frac >= RS_BSTAGE_MIN) {
                     h->rows_per_tile = Rb;
                     h->capz = capz_for(Rb);
-                    h->capb = (int)capb;
+                    h->capb = (int)std::min<long long>(capb_try, (long long)((cnt[1] + 15) & ~15ULL));
+                    break;
                 }
             }
         }
