@@ -61,7 +61,8 @@ constexpr int kNumSMs = 148;
 #define RS_GDIV 2  // row split, 16..32 vector lanes per row: split the row over lanes/RS_GDIV lanes
 #endif
 #ifndef TE_CARVE
-#define TE_CARVE 1  // request the minimal shared-memory carveout (maximal L1) for the resident CTAs
+#define TE_CARVE 0  // 1: request the minimal shared-memory carveout (maximal L1); measured neutral to slower
+                    // (the SM re-partitions when the next kernel wants another split)
 #endif
 #ifndef RS_STAGES
 #define RS_STAGES 3
@@ -88,6 +89,9 @@ constexpr int kPairU = RSP_U;
 #ifndef RS_BSTAGE
 #define RS_BSTAGE 1  // row split: stage compact B row spans into shared memory with TMA (plan-time measured)
 #endif
+#ifndef RS_BSTAGE_MIN_ROW
+#define RS_BSTAGE_MIN_ROW 256  // stage B only for rows of >= 256 bytes (n >= 64 fp32); below, L1 serves
+#endif                         // the short rows better (measured: banded n=16/32 slower when staged)
 #ifndef RS_BSTAGE_MIN
 #define RS_BSTAGE_MIN 0.5  // stage B when at least this fraction of the nonzeros lies in compact tiles
 #endif
@@ -616,7 +620,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         h->capb = 0;
         h->bspan_compact = -1.0;
         const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
-        if (RS_BSTAGE && h->nnz > 0 && (n * elem) % 16 == 0) {
+        if (RS_BSTAGE && h->nnz > 0 && (n * elem) % 16 == 0 && n * elem >= RS_BSTAGE_MIN_ROW) {
             // B staging: the largest tile height R_b <= R whose tiles' B row spans fit
             // the shared memory left next to the CSR slice (3 stages x 2 CTAs per SM) for at least
             // RS_BSTAGE_MIN of the nonzeros; the per-stage B slot is then sized to the largest
