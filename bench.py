@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--items", type=int, default=0)
     ap.add_argument("--row-partition", type=int, default=1, help="multi-GPU: 0 nnz-balanced, 1 merge-path")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--gather-c", action="store_true", help="multi-GPU: also time an all-gather of C")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
@@ -316,6 +317,41 @@ def main():
     else:
         flops_all, balg_all, nnz_all = flops_local, float(balg), float(p.nnz)
     total_ms, dom_total_ms = float(tot[0]), float(tot[1])
+
+    # warm-L2 companion number (the cold, flushed figure is primary): same steps, no flush
+    warm_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(min(args.steps, 20))]
+    for evs in warm_sets:
+        for e in evs:
+            e.record()
+    torch.cuda.synchronize()
+    for evs in warm_sets:
+        step(evs)
+    torch.cuda.synchronize()
+    op.set_timing_events([])
+    warm_ms = sorted(ev[0].elapsed_time(ev[-1]) for ev in warm_sets)[len(warm_sets) // 2]
+
+    # optional all-gather of C, timed separately from the SpMM
+    allgather_ms = None
+    if world > 1 and args.gather_c:
+        rows = torch.tensor([p.m], dtype=torch.int64, device=dev)
+        allr = [torch.empty_like(rows) for _ in range(world)]
+        tdist.all_gather(allr, rows)
+        mx = max(int(r.item()) for r in allr)
+        pad = torch.zeros(mx, n, dtype=C.dtype, device=dev)
+        pad[:p.m] = C
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        tdist.all_gather(parts, pad)  # warm-up
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        tdist.all_gather(parts, pad)
+        g1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([g0.elapsed_time(g1)], device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        allgather_ms = float(t.item())
+        del parts, pad
     ms_per_step = total_ms / args.steps
     value = flops_all * args.steps / (total_ms / 1e3) / 1e9
     gbs = balg_all * args.steps / (total_ms / 1e3) / 1e9
@@ -352,10 +388,11 @@ def main():
                        "partition": args.partition if chosen == "merge" else None,
                        "l2": "flushed before every timed step (2x L2 bytes written)" if not args.no_flush
                        else "not flushed",
-                       "parallelism": f"row-block x{world}", "bcast_B_ms": bcast_ms,
+                       "parallelism": f"row-block x{world}", "bcast_B_ms": bcast_ms, "allgather_C_ms": allgather_ms,
                        "mean_row_length": info["mean_row_length"], "max_row_length": info["max_row_length"]},
             "hbm_gbs_alg": round(gbs, 1), "bytes_alg_per_step": int(balg_all),
             "frac_of_roofline_step": round(gbs / peak, 4),
+            "warm_l2_ms_per_step": round(warm_ms, 5), "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
             "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": round(achieved, 1), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "bytes_alg_per_launch": balg,

@@ -277,12 +277,6 @@ cudaError_t launch_tile(TileParams P, cudaStream_t st) {
     else kfn = k_tile<T, SR, MODE, V, G, NV, U>;
     size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G), MODE == MODE_MERGE,
                                 MODE == MODE_ROWSPLIT ? P.capb : 0);
-    if (MODE == MODE_MERGE && G == 32) {  // + per-warp cp.async rings of gathered B rows
-        const int SB = 32 * V * NV * (int)sizeof(T);
-        smem = (smem + 15) & ~(size_t)15;
-        P.ring_off = (int)smem;
-        smem += (size_t)TE_CWARPS * mg_ring_slots(SB) * SB;
-    }
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
 #if TE_CARVE

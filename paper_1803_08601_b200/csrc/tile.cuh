@@ -61,7 +61,6 @@ struct TileParams {
     int capr, capz;     // elements per buffer: row offsets / (col, val)
     unsigned pf_bytes;  // bytes of each B row to prefetch into L2 ahead of the consumers (0 = off)
     int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
-    int ring_off;       // merge: byte offset of the per-warp B-row rings in dynamic shared memory
     int capb;           // rowsplit: bytes per stage for the tile's B row span (0 = B is gathered from global)
 };
 
@@ -141,29 +140,6 @@ template <> __device__ __forceinline__ void lds_vpred<4>(unsigned (&o)[4], uint3
                  : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "r"(a), "r"((int)pred));
 }
 
-#ifndef MG_RING_BYTES
-#define MG_RING_BYTES 0  // merge: bytes of gathered B rows per warp in a cp.async ring (0 = registers; slower so far)
-#endif
-// slots of the cp.async ring for a worker covering SB bytes of a B row (multiple of 8, >= 16)
-__host__ __device__ constexpr int mg_ring_slots(int SB) {
-    return MG_RING_BYTES == 0 ? 0 : ((MG_RING_BYTES / SB) / 8 * 8 < 16 ? 16 : (MG_RING_BYTES / SB) / 8 * 8);
-}
-
-#ifndef B_L2_HINT
-#define B_L2_HINT 0  // 1: gather B rows with an L2 evict_last cache policy (keep hot B rows resident)
-#endif
-template <int VEC> __device__ __forceinline__ void ldg_nc(unsigned (&o)[VEC], const void* p, uint64_t pol) {
-    if constexpr (B_L2_HINT == 0) {
-        ldg_vec<VEC>(o, p);
-    } else if constexpr (VEC == 4) {
-        asm volatile("ld.global.nc.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
-                     : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p), "l"(pol));
-    } else if constexpr (VEC == 2) {
-        asm volatile("ld.global.nc.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;" : "=r"(o[0]), "=r"(o[1]) : "l"(p), "l"(pol));
-    } else {
-        asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(o[0]) : "l"(p), "l"(pol));
-    }
-}
 
 // accumulator of VEC*NV columns for one lane
 template <typename T, int SR, int VEC, int NV> struct Acc {
@@ -439,7 +415,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
     for (int v = 0; v < NV; ++v) boff[v] = colok[v] ? (uint32_t)(cofs[v] * sizeof(T)) : 0u;
     T* Cl = static_cast<T*>(P.C) + gl * VEC;
     const unsigned ldb_bytes = P.ldb_bytes;
-    const uint64_t bpol = B_L2_HINT ? policy_evict_last() : 0;
 
     auto gather = [&](unsigned (&o)[NV][VEC], int c, bool ok) {
 #pragma unroll
@@ -447,7 +422,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
     };
     auto gather_full = [&](unsigned (&o)[NV][VEC], int c) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) ldg_nc<VEC>(o[v], Blv[v] + (size_t)(unsigned)c * ldb_bytes, bpol);
+        for (int v = 0; v < NV; ++v) ldg_vec<VEC>(o[v], Blv[v] + (size_t)(unsigned)c * ldb_bytes);
     };
     auto store_row = [&](long long row, const Acc<T, SR, VEC, NV>& acc, bool ok) {
         T* crow = Cl + row * P.ldc;
@@ -512,21 +487,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                         unsigned bv[U][NV][VEC];
                         unsigned cu[U], av[U];
                         const bool full_b = rem >= U;
-#ifdef RS_SHFL
-                        if (G >= 2 * U && __all_sync(FULL, full_b)) {  // one LDS per lane + shuffles
-                            const unsigned x = lds_u32(gl < U ? cs + 4u * (p0 + gl) : vs + 4u * (p0 + gl - U));
-#pragma unroll
-                            for (int u = 0; u < U; ++u) {
-                                cu[u] = __shfl_sync(FULL, x, u, G);
-                                av[u] = __shfl_sync(FULL, x, U + u, G);
-                            }
-#pragma unroll
-                            for (int u = 0; u < U; ++u) GF(kS, bv[u], (int)cu[u]);
-#pragma unroll
-                            for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(av[u]), bv[u]);
-                            continue;
-                        }
-#endif
                         if (__all_sync(FULL, full_b && ((cs & 15u) == 0))) {  // full, 16B-aligned: LDS.128
 #pragma unroll
                             for (int u = 0; u < U; u += 4) {
@@ -788,86 +748,13 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 ++r;
                 e = (r < m) ? Eb[r] : 0x7fffffff;
             };
-          constexpr int SBR = 32 * VEC * NV * (int)sizeof(T);
-          if constexpr (G == 32 && mg_ring_slots(SBR) > 0) {
-            // gathered B rows land in a per-warp shared-memory ring via cp.async (LDGSTS), 8 nonzeros
-            // per commit group, D nonzeros in flight: the memory-level parallelism is bounded by shared
-            // memory instead of registers (R-MAT-like gathers are latency bound)
-            constexpr int LB = VEC * (int)sizeof(T);
-            constexpr int D = mg_ring_slots(SBR);
-            constexpr int NB = D / 8;
-            const uint32_t ring = smem_u32(smem) + (uint32_t)P.ring_off + (uint32_t)(warp * D * SBR) + lane * LB;
-            const uint32_t col_s = smem_u32(COL) - 4u * (uint32_t)inf.zbase;
-            const uint32_t val_s = smem_u32(VAL) - 4u * (uint32_t)inf.zbase;
-            int qi = q;
-            auto issue_batch = [&]() {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int qq = qi + u;
-                    if (qq < jb) {
-                        const unsigned c = lds_u32(col_s + 4u * (uint32_t)qq);
-                        const uint32_t dst = ring + (uint32_t)(qq % D) * SBR;
-#pragma unroll
-                        for (int v = 0; v < NV; ++v)
-                            cp_async<LB>(dst + v * 32 * LB, Blv[v] + (size_t)c * ldb_bytes);
-                    }
-                }
-                cp_async_commit();
-                qi += 8;
-            };
-#pragma unroll
-            for (int k = 0; k < NB; ++k) issue_batch();
-            while (q < jb) {
-                cp_async_wait<NB - 1>();  // this lane's copies of the oldest batch have landed
-                const int cnt = min(8, jb - q);
-                if (cnt == 8 && q + 8 <= e) {  // whole batch inside the current row
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int qq = q + u;
-                        unsigned bv[NV][VEC];
-#pragma unroll
-                        for (int v = 0; v < NV; ++v) lds_vec<VEC>(bv[v], ring + (uint32_t)(qq % D) * SBR + v * 32 * LB);
-                        accs[u % NA].mac(from_bits<T>(lds_u32(val_s + 4u * (uint32_t)qq)), bv);
-                    }
-                    dirty = true;
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        if (u < cnt) {
-                            const int qq = q + u;
-                            while (e <= qq) flush();  // rows ending before nonzero qq (rows first on ties)
-                            unsigned bv[NV][VEC];
-#pragma unroll
-                            for (int v = 0; v < NV; ++v)
-                                lds_vec<VEC>(bv[v], ring + (uint32_t)(qq % D) * SBR + v * 32 * LB);
-                            accs[u % NA].mac(from_bits<T>(lds_u32(val_s + 4u * (uint32_t)qq)), bv);
-                            dirty = true;
-                        }
-                    }
-                }
-                q += cnt;
-                issue_batch();
-            }
-            cp_async_wait<0>();
-            while (r < ib) flush();
-          } else if constexpr (G == 32) {
-#ifndef MG_PF
-#define MG_PF 0
-#endif
+          if constexpr (G == 32) {
             while (q < jb) {
                 const int cnt = min(U, jb - q);
                 unsigned bv[U][NV][VEC];
                 T av[U];
                 const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(q - inf.zbase);
                 const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(q - inf.zbase);
-                if (MG_PF > 0) {
-                    // software prefetch into L2 of the B rows gathered MG_PF nonzeros ahead: turns the
-                    // DRAM misses of the next batch into L2 hits without holding registers
-                    const int pq = q + MG_PF;
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (pq + u < jb) prefetch_l2(Bl + (size_t)lds_u32(cs + 4u * (MG_PF + u)) * ldb_bytes);
-                }
                 unsigned cu[U], au[U];
                 if (cnt == U && q + U <= e) {  // full batch inside the current row: no row end to check
                     if ((cs & 15u) == 0) {
