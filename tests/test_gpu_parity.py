@@ -454,3 +454,41 @@ def test_b_staging_plan_decision():
         assert inf["b_staging"] == want, inf
         assert (inf["bspan_compact"] > 0.9) == bool(want)
         op.close()
+
+
+# ------------------------------------------------------------------------------------------------
+# randomized shapes: every path against the oracle on seeded random CSR / n / ld / algo / partition
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", range(48))
+def test_randomized_parity(case):
+    rng = np.random.default_rng(9000 + case)
+    m = int(rng.integers(1, 5000))
+    k = int(rng.integers(1, 5000))
+    shape = case % 4
+    if shape == 0:    # uniform short rows
+        lens = rng.integers(0, 24, m)
+    elif shape == 1:  # skewed: a few long rows, many empty
+        lens = np.where(rng.random(m) < 0.6, 0, rng.integers(1, 8, m))
+        lens[rng.integers(0, m, 3)] = rng.integers(500, 4000, 3)
+    elif shape == 2:  # banded around the diagonal (compact B spans)
+        lens = None
+    else:             # lognormal
+        lens = np.minimum(np.round(rng.lognormal(1.5, 1.0, m)).astype(np.int64), 2000)
+    if lens is None:
+        w = int(rng.integers(1, 20))
+        p = synth.banded(m, lo=w // 2, hi=w - w // 2 - 1)
+    else:
+        lens = np.minimum(lens, k)
+        p = synth.explicit_lengths(m, k, [int(x) for x in lens], seed=case)
+    n = int(rng.choice([1, 2, 3, 4, 5, 8, 12, 16, 24, 32, 40, 48, 63, 64, 96, 127, 128]))
+    kind = synth.KINDS[case % len(synth.KINDS)]
+    algo = ["rowsplit", "merge", "auto"][(case // 4) % 3]
+    kw = {}
+    if algo == "merge":
+        kw = {"partition": ["merge_path", "nonzero_split"][case % 2],
+              "items_per_cta": int(rng.choice([256, 512, 1024, 2048, 4096]))}
+    ldb = n + int(rng.choice([0, 0, 4, 7])) if case % 5 else None
+    ldc = n + int(rng.choice([0, 3])) if case % 3 else None
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, seed=case, ldb=ldb, ldc=ldc)
+    run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd, **kw)
+    check(p, kind, n, val, Bh, Cd)
