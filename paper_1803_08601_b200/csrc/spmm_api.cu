@@ -70,6 +70,9 @@ constexpr int kNumSMs = 148;
 #ifndef RS_TILE_NNZ
 #define RS_TILE_NNZ 2048  // row split: target nonzeros per row tile
 #endif
+#ifndef RS_CAPZ_MAX
+#define RS_CAPZ_MAX 8200  // row split: most nonzeros a staged tile slice holds (+8 slack)
+#endif
 #ifndef RS_ZF
 #define RS_ZF 12  // row split: staged capacity = RS_ZF/10 x the tile's expected nonzeros
 #endif
@@ -581,7 +584,11 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true);
             const long long groups = (long long)num_sms() * 2 * TE_CWARPS * (32 / rc.G);  // resident row groups
             const bool few_rows = h->m < 2 * groups;
-            pick = (skewed || few_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
+            // rows so long that even a 16-row tile overflows the staged CSR slice: the row-split kernel
+            // would stream A from global per row group (measured 2.5x slower than merge at d = 1000,
+            // profiles/r01_density_sweep.txt), while merge path stages fixed-size slices at any d
+            const bool long_rows = RS_ZF / 10.0 * 16.0 * d > (double)(RS_CAPZ_MAX - 8);
+            pick = (skewed || few_rows || long_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
         }
     }
     h->chosen = pick;
@@ -606,7 +613,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
 #endif
         auto capz_for = [&](int rows) {
             long long z = (long long)std::ceil(RS_ZF / 10.0 * rows * dd);
-            z = std::max<long long>(1024, std::min<long long>(z, 8192));
+            z = std::max<long long>(1024, std::min<long long>(z, RS_CAPZ_MAX - 8));
             return (int)(((z + 3) & ~3LL) + 8);
         };
         h->rows_per_tile = R;

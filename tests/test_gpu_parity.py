@@ -269,6 +269,16 @@ def test_heuristic_choice_matches_oracle_rule():
     op.close()
 
 
+def test_auto_picks_merge_for_rows_too_long_to_stage():
+    # 1.2 x 16 x d > 8192 <=> d > 426: a 16-row tile no longer fits the staged slice
+    for d, want in ((400, "rowsplit"), (450, "merge")):
+        p = synth.uniform_rows(40000, 20000, d, d)
+        vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
+        op = S.CsrSpmm(p.row_offsets.to(DEV), p.col_indices.to(DEV), vd, p.k)
+        assert op.plan(64, "auto") == want
+        op.close()
+
+
 def test_abi_errors_on_device():
     p = synth.uniform_rows(100, 100, 4, 2)
     vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
