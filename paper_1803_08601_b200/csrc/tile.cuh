@@ -616,7 +616,13 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                             unsigned cu[U], av[U], aq[U];
                             const uint32_t ca = colz + 4u * (uint32_t)(sL + p0);
                             const uint32_t va = valz + 4u * (uint32_t)(sL + p0);
+                            // mask bits of Q entries p0 - delta .. p0 - delta + U - 1 (p0 - delta < 32)
+                            const int j0 = p0 - delta;
+                            const uint32_t mw = (j0 >= 0) ? (mask >> j0) : (j0 > -32 ? (mask << -j0) : 0u);
                             if (U % 4 == 0 && __all_sync(FULL, rem >= U && (ca & 15u) == 0)) {
+                                // full batch for every group: unpredicated loads; Q's values are read
+                                // unconditionally (eL + j0 + u >= sL stays inside the stage buffer) and
+                                // used only where the mask says the entry is paired
 #pragma unroll
                                 for (int u = 0; u < U; u += 4) {
                                     const uint4 c4 = lds_u128(ca + 4u * u);
@@ -624,16 +630,22 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                                     cu[u] = c4.x; cu[u + 1] = c4.y; cu[u + 2] = c4.z; cu[u + 3] = c4.w;
                                     av[u] = a4.x; av[u + 1] = a4.y; av[u + 2] = a4.z; av[u + 3] = a4.w;
                                 }
-                            } else {
+#pragma unroll
+                                for (int u = 0; u < U; ++u) aq[u] = lds_u32(valz + 4u * (uint32_t)(eL + j0 + u));
+#pragma unroll
+                                for (int u = 0; u < U; ++u) GF(kS, bv[u], (int)cu[u]);
 #pragma unroll
                                 for (int u = 0; u < U; ++u) {
-                                    cu[u] = lds_pred(ca + 4u * u, u < rem);
-                                    av[u] = lds_pred(va + 4u * u, u < rem);
+                                    accL.mac(from_bits<T>(av[u]), bv[u]);
+                                    if ((mw >> u) & 1u) accQ.mac(from_bits<T>(aq[u]), bv[u]);
                                 }
+                                continue;
                             }
-                            // mask bits of Q entries p0 - delta .. p0 - delta + U - 1
-                            const int j0 = p0 - delta;
-                            const uint32_t mw = (j0 >= 0) ? (j0 < 32 ? (mask >> j0) : 0u) : (mask << (-j0 < 32 ? -j0 : 31)) & (-j0 < 32 ? 0xffffffffu : 0u);
+#pragma unroll
+                            for (int u = 0; u < U; ++u) {
+                                cu[u] = lds_pred(ca + 4u * u, u < rem);
+                                av[u] = lds_pred(va + 4u * u, u < rem);
+                            }
 #pragma unroll
                             for (int u = 0; u < U; ++u)
                                 aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j0 + u), (mw >> u) & 1u);
