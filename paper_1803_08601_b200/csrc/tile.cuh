@@ -89,24 +89,33 @@ __host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, in
 }
 
 // stage global src[begin, end) (4-byte elements, arr_len elements in the array) at dst; returns the
-// global index stored at dst[0] and adds TMA bytes to *tx.  Only the final partial 16-byte group of
-// the array is loaded with plain loads (never read past arr_len).
+// global index of the element stored at dst[0] and adds TMA bytes to *tx.  The TMA copy covers the
+// 16-byte aligned ADDRESS range around [begin, end) -- src itself may be any 4-byte aligned pointer
+// (e.g. a row block sliced out of a larger CSR), so the returned index can be below begin (down to
+// begin - 3, or -3 at the array start: same 16-byte granule, never another page).  The part past the
+// array's last full granule is loaded with plain loads (never read past arr_len).
 __device__ __forceinline__ int te_stage(void* dst, const void* src, long long begin, long long end, long long arr_len,
                                         uint64_t* bar, uint64_t pol, uint32_t* tx) {
-    const long long a_al = begin & ~3LL;
-    if (end <= begin) return (int)a_al;
-    long long b_al = (end + 3) & ~3LL;
-    const long long lim = arr_len & ~3LL;
+    const long long mis = (long long)((reinterpret_cast<uintptr_t>(src) >> 2) & 3);  // elements past a granule
+    const unsigned* srca = static_cast<const unsigned*>(src) - mis;                     // 16-byte aligned
+    const long long a_al = (begin + mis) & ~3LL;  // indices into srca
+    if (end <= begin) return (int)(a_al - mis);
+    long long b_al = (end + mis + 3) & ~3LL;
+    const long long lim = (arr_len + mis) & ~3LL;
     if (b_al > lim) b_al = lim;
     if (b_al > a_al) {
         const uint32_t bytes = (uint32_t)((b_al - a_al) * 4);
-        tma_load_1d(dst, static_cast<const unsigned*>(src) + a_al, bytes, bar, pol);
+        tma_load_1d(dst, srca + a_al, bytes, bar, pol);
         *tx += bytes;
     }
-    for (long long p = (b_al > begin ? b_al : begin); p < end; ++p)
-        static_cast<unsigned*>(dst)[p - a_al] = static_cast<const unsigned*>(src)[p];
-    return (int)a_al;
+    for (long long p = (b_al - mis > begin ? b_al - mis : begin); p < end; ++p)
+        static_cast<unsigned*>(dst)[p + mis - a_al] = static_cast<const unsigned*>(src)[p];
+    return (int)(a_al - mis);
 }
+
+// 16-byte granule phase of a 4-byte element array (TMA copies of two arrays share an index base only
+// when their phases agree)
+__device__ __forceinline__ int te_phase(const void* p) { return (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3); }
 
 // predicated vector gather of B (no branch): o valid only if pred
 template <int VEC> __device__ __forceinline__ void ldg_pred(unsigned (&o)[VEC], const void* p, bool pred);
@@ -301,6 +310,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             if (lane == 0) mbar_arrive_expect_tx(&full[pb], btx);
         };
         const bool bstage = MODE == MODE_ROWSPLIT && P.capb > 0;
+        const bool val_tma = te_phase(P.col) == te_phase(P.val);
         int pend = -1;  // B staging: tile index whose CSR slice is in flight
         for (int c = blockIdx.x; c < P.num_ranges; c += gridDim.x) {
             long long rs, zs, re, ze;
@@ -330,6 +340,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 int b;
                 acquire(b);
                 uint64_t* csr_bar = bstage ? &landed[b] : &full[b];
+                uint32_t ptx_tx = 0;  // lane 0: TMA bytes of a tile whose values the warp copies
                 if (lane == 0) {
                     uint32_t tx = 0;
                     TileInfo inf;
@@ -348,13 +359,29 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                     }
                     if (staged) {
                         inf.zbase = te_stage(COL_of(b), P.col, cz, nz, P.nnz, csr_bar, pol, &tx);
-                        te_stage(VAL_of(b), P.val, cz, nz, P.nnz, csr_bar, pol, &tx);
+                        // values share the column indices' index base when both arrays have the same
+                        // 16-byte phase (always for arrays sliced at the same offset); otherwise the
+                        // warp copies them below with plain loads
+                        if (val_tma) te_stage(VAL_of(b), P.val, cz, nz, P.nnz, csr_bar, pol, &tx);
                     } else {
                         inf.zbase = 0;
                     }
                     inf.flags = (first ? 1 : 0) | (last ? 2 : 0) | (staged ? 4 : 0);
                     *INFO_of(b) = inf;
-                    mbar_arrive_expect_tx(csr_bar, tx);
+                    if (val_tma || !staged) mbar_arrive_expect_tx(csr_bar, tx);
+                    else ptx_tx = tx;
+                }
+                if (!val_tma) {
+                    const TileInfo* ip = INFO_of(b);
+                    __syncwarp();
+                    if (ip->flags & 4) {
+                        const int zb = ip->zbase;
+                        for (long long p = cz + lane; p < nz; p += 32)
+                            static_cast<unsigned*>(static_cast<void*>(VAL_of(b)))[p - zb] =
+                                static_cast<const unsigned*>(P.val)[p];
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_expect_tx(csr_bar, ptx_tx);
+                    }
                 }
                 __syncwarp();
                 if (bstage) {

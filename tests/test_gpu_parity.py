@@ -502,3 +502,52 @@ def test_randomized_parity(case):
     val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, seed=case, ldb=ldb, ldc=ldc)
     run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd, **kw)
     check(p, kind, n, val, Bh, Cd)
+
+
+# ------------------------------------------------------------------------------------------------
+# CSR arrays that are views at arbitrary 4-byte offsets (row blocks sliced out of a larger matrix, as
+# the multi-GPU partition does): the TMA staging must align by address, and values whose 16-byte
+# phase differs from the column indices' are copied by the producer warp
+# ------------------------------------------------------------------------------------------------
+def _offset_view(t, off):
+    buf = torch.empty(t.numel() + 4, dtype=t.dtype, device=DEV)
+    buf[off:off + t.numel()] = t
+    return buf[off:off + t.numel()]
+
+
+@pytest.mark.parametrize("offs", [(0, 1, 1), (0, 2, 2), (0, 3, 3), (1, 1, 2), (3, 2, 0), (2, 0, 3)])
+@pytest.mark.parametrize("algo", ["rowsplit", "merge"])
+@pytest.mark.parametrize("pat", ["banded", "lognormal"])
+@pytest.mark.parametrize("kind", ["f32_plus_times", "i32_min_plus"])
+def test_misaligned_csr_views(offs, algo, pat, kind):
+    p = synth.banded(3001) if pat == "banded" else synth.lognormal_rows(3001, 2000, 7.92, 19)
+    n = 64
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    o_ro, o_ci, o_v = offs
+    ro2, ci2, vd2 = _offset_view(ro, o_ro), _offset_view(ci, o_ci), _offset_view(vd, o_v)
+    assert ci2.data_ptr() % 16 == 4 * o_ci
+    run_gpu(p, kind, n, algo, ro2, ci2, vd2, Bd, Cd)
+    check(p, kind, n, val, Bh, Cd)
+
+
+def test_row_block_slices_match_full_matrix():
+    """The multi-GPU local step: row blocks sliced (views, offsets not multiples of 4) out of one CSR,
+    each multiplied on its own, reassemble C of the whole matrix bit-exactly for an exact semiring."""
+    from paper_1803_08601_b200 import dist as D
+    p = synth.rmat(13, 8, 21)
+    kind, n = "i32_plus_times", 48
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    run_gpu(p, kind, n, "auto", ro, ci, vd, Bd, Cd)
+    full = Cd.cpu()
+    for parts, mode in ((3, 0), (5, 1), (8, 1)):
+        bounds = D.partition_rows(p.row_offsets, parts, mode)
+        for r in range(parts):
+            r0, r1 = bounds[r], bounds[r + 1]
+            bro, bci, bvd = D.slice_rows(ro, ci, vd, r0, r1)
+            for algo in ("rowsplit", "merge"):
+                op = S.CsrSpmm(bro, bci, bvd, p.k)
+                op.plan(n, algo, "plus_times")
+                C = op.execute(Bd)
+                torch.cuda.synchronize()
+                op.close()
+                assert torch.equal(C.cpu(), full[r0:r1]), (parts, mode, r, algo)
