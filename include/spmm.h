@@ -118,6 +118,8 @@ typedef struct {
  *   non-decreasing offsets, row_offsets[m] == nnz and 0 <= col < k (else SPMM_ERR_INVALID_CSR).
  *   Without it the CSR is trusted.  m == 0 or nnz == 0 is allowed (pointers may then be NULL
  *   except row_offsets when m > 0).  k == 0 requires nnz == 0.
+ *   The three arrays may be views at any 4-byte offset (e.g. a row block of a larger CSR): the kernels
+ *   stage them with TMA by address, reading at most to the enclosing 16-byte granules.
  *   *out receives a new handle (owned by the caller, free with spmm_csr_destroy).
  */
 SPMM_API spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz,
@@ -129,7 +131,9 @@ SPMM_API spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int6
  *   algo_or_auto: force ROWSPLIT / MERGE, or AUTO (§5.4 heuristic).
  *   threshold <= 0 -> 9.35.  *workspace_bytes receives the device workspace size
  *   execute() needs (0 for row split); *chosen receives ROWSPLIT or MERGE.  Either out pointer may
- *   be NULL.  Plan with AUTO policy enqueues one reduction on `stream` and synchronises it.
+ *   be NULL.  Plan enqueues small measurement kernels on `stream` and synchronises it: the maximum
+ *   row length (AUTO policy) and, for the row-split kernel with n * 4 >= 256 bytes, the compactness
+ *   of the row tiles' B spans (B staging, see spmm_plan_info.b_staging).  Plan once, execute often.
  */
 SPMM_API spmm_status spmm_csr_plan(spmm_csr_t h, int32_t n, spmm_algo algo_or_auto, spmm_semiring sr,
                           double threshold, void* stream, size_t* workspace_bytes, spmm_algo* chosen);
