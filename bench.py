@@ -194,6 +194,43 @@ def oracle_time_sample(p_cpu: synth.CsrPattern, val_cpu, B_cpu, n: int, budget_s
     return fl * runs / tot / 1e9, tot / runs, R, fl, runs
 
 
+def oracle_one_thread(p_cpu, val_cpu, B_np, n, budget_s):
+    """The oracle with OpenMP limited to one thread (restored afterwards); (GFLOP/s, rows) or None."""
+    import ctypes
+    import oracle
+    try:
+        gomp = ctypes.CDLL("libgomp.so.1")
+        prev = gomp.omp_get_max_threads()
+    except OSError:
+        return None
+    ro = p_cpu.row_offsets.numpy()
+    col = p_cpu.col_indices.numpy()
+    vals = val_cpu.numpy()
+    gomp.omp_set_num_threads(1)
+    try:
+        R = min(p_cpu.m, 2048)
+        while True:
+            z = int(ro[R])
+            t0 = time.perf_counter()
+            oracle.spmm("f32_plus_times", R, p_cpu.k, n, ro[:R + 1], col[:z], vals[:z], B_np, ldb=n)
+            dt = time.perf_counter() - t0
+            if dt > 0.25 * budget_s or R >= p_cpu.m:
+                return 2.0 * z * n / dt / 1e9, R
+            R = min(p_cpu.m, R * 4)
+    finally:
+        gomp.omp_set_num_threads(prev)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -377,6 +414,12 @@ def main():
         cpu = {"value": round(gfl, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
                "sample": f"oracle (plain C, fp64 accumulation + |A||B| bound, OpenMP) on the first {R} of {p.m} "
                          f"rows of the same workload ({fl / 2 / n:.0f} nnz) x {runs} runs, {dt:.3f} s per run"}
+        # the oracle at 1 thread too (a smaller sample of the same rows)
+        g1 = oracle_one_thread(p_cpu, vals.cpu(), B.cpu().numpy(), n, budget_s=4.0)
+        if g1 is not None:
+            cpu["value_1thread"] = round(g1[0], 4)
+            cpu["sample_1thread"] = f"first {g1[1]} rows, 1 OpenMP thread"
+            cpu["cpu_model"] = cpu_model()
 
     if rank == 0:
         out = {
