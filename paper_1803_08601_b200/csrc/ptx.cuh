@@ -88,6 +88,13 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 // predicated shared-memory load (no branch); o unchanged/undefined when !pred
+// shared-memory atomic add with acquire-release semantics at CTA scope; returns the old value
+__device__ __forceinline__ int smem_atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ unsigned lds_pred(uint32_t saddr, bool pred) {
     unsigned v;
     asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; mov.b32 %0, 0; @q ld.shared.b32 %0, [%1];}"

@@ -960,15 +960,15 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 int* srow = CrowS + b * NWK;
                 int* sflag = CflagS + b * NWK;
                 publish(slots, srow, sflag);
+                // hand-off: __syncwarp orders the warp's slot writes before lane 0's acq_rel atomic
+                // (release); the warp whose increment completes the count acquires every earlier
+                // release and passes the ordering on to its lanes with __syncwarp
                 __syncwarp();
                 int last = 0;
-                if (lane == 0) {
-                    __threadfence_block();
-                    last = (atomicAdd(&Ccnt[b], 1) == TE_CWARPS - 1) ? 1 : 0;
-                }
+                if (lane == 0) last = (smem_atom_add_acq_rel(&Ccnt[b], 1) == TE_CWARPS - 1) ? 1 : 0;
                 last = __shfl_sync(FULL, last, 0);
                 if (last) {
-                    __threadfence_block();
+                    __syncwarp();
                     T open[4];
                     bool open_any;
                     resolve(slots, srow, sflag, open, open_any);
