@@ -326,16 +326,10 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
     cudaError_t e;
     if (h->pairing) {
         e = cudaErrorNotSupported;
-#ifdef RSP_WIDE
-        if (cfg.NV == 2 && cfg.G <= 8) {  // pairs: a row over twice the lanes, one vector block each
-            cfg.G *= 2;
-            cfg.NV = 1;
-        }
-#endif
 #define RSP_CASE(V, G_, NV_) \
     case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kPairU, true>(P, st); break;
         switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
-            RSP_CASE(4, 2, 1) RSP_CASE(4, 4, 1) RSP_CASE(4, 8, 1) RSP_CASE(4, 8, 2) RSP_CASE(4, 16, 2) RSP_CASE(4, 16, 1)
+            RSP_CASE(4, 2, 1) RSP_CASE(4, 4, 1) RSP_CASE(4, 8, 1) RSP_CASE(4, 8, 2) RSP_CASE(4, 16, 2)
             default: break;
         }
 #undef RSP_CASE
@@ -609,7 +603,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         while (R * 2 <= 4096 && R * 2 * dd <= (double)RS_TILE_NNZ) R *= 2;
         R = std::max(16, std::min(R, 1024));
 #ifdef RS_R_FORCE
-        R = RS_R_FORCE;
+        R = RS_R_FORCE;  // tuning knob: fixed tile height
 #endif
         auto capz_for = [&](int rows) {
             long long z = (long long)std::ceil(RS_ZF / 10.0 * rows * dd);
