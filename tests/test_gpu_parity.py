@@ -551,3 +551,51 @@ def test_row_block_slices_match_full_matrix():
                 torch.cuda.synchronize()
                 op.close()
                 assert torch.equal(C.cpu(), full[r0:r1]), (parts, mode, r, algo)
+
+
+# ------------------------------------------------------------------------------------------------
+# BASELINE configs 1 and 2 at full size, EVERY row against the oracle (SURVEY.md §8(d) parity
+# coverage), in the launch configuration bench.py times (AUTO) and with each kernel forced
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("algo", ["auto", "rowsplit", "merge"])
+def test_full_size_configs_every_row(cfg, algo):
+    p = synth.config_pattern(cfg, device=DEV).to("cpu")
+    kind, n = "f32_plus_times", 64
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, seed=synth.STRUCT_SEED + cfg)
+    run_gpu(p, kind, n, algo, ro, ci, vd, Bd, Cd)
+    check(p, kind, n, val, Bh, Cd)
+
+
+def test_config4_rmat26_sampled_rows():
+    """BASELINE configs[4] (R-MAT scale 26, ~1.06e9 nonzeros, n = 64) in the bench launch configuration:
+    the 1,024 longest rows, the rows around every merge-CTA boundary of a deterministic subset, and 2^20
+    seeded random rows, against the oracle (SURVEY.md §8(d) config 5 sample)."""
+    p = synth.config_pattern(4, device=DEV)
+    kind, n = "f32_plus_times", 64
+    seed = synth.STRUCT_SEED + 4
+    vd = synth.values(p.nnz, seed + 100, kind, device=DEV)
+    Bd = synth.dense(p.k, n, seed + 200, kind, device=DEV)
+    Cd = torch.full((p.m, n), float("nan"), device=DEV)
+    op = S.CsrSpmm(p.row_offsets, p.col_indices, vd, p.k)
+    chosen = op.plan(n, "auto")
+    info = op.info()
+    op.execute(Bd, Cd)
+    torch.cuda.synchronize()
+    op.close()
+    assert chosen == "merge" and not torch.isnan(Cd).any()
+    lens = (p.row_offsets[1:] - p.row_offsets[:-1]).to(torch.int64)
+    longest = torch.topk(lens, 1024).indices.cpu()
+    g = torch.Generator().manual_seed(4)
+    rand = torch.randint(0, p.m, (1 << 20,), generator=g)
+    # rows at merge-path CTA boundaries (items_per_cta = 2048): diagonal c*2048 -> row ~ searchsorted
+    items = info["items_per_cta"]
+    diag = torch.arange(0, p.m + p.nnz, items * 997, dtype=torch.int64)
+    ro64 = p.row_offsets.to(torch.int64).cpu()
+    brow = torch.searchsorted(ro64 + torch.arange(p.m + 1), diag).clamp(0, p.m - 1)
+    rows = torch.unique(torch.cat([longest, rand, brow, (brow + 1).clamp(max=p.m - 1), (brow - 1).clamp(min=0)]))
+    pc = p.to("cpu")
+    Cref, bound = oracle.spmm(kind, p.m, p.k, n, pc.row_offsets, pc.col_indices, vd.cpu(), Bd.cpu(), rows=rows.numpy())
+    C = Cd.cpu().numpy()[rows.numpy()]
+    ok, worst, idx = oracle.check_f32(C, Cref, bound, TOL)
+    assert ok, f"worst |err|/bound {worst} at {idx}"
