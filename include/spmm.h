@@ -70,7 +70,8 @@ typedef struct {
     int32_t policy;          /* spmm_policy.  PAPER: merge iff d < threshold.
                                 AUTO (default): B200 refit of §5.4 -- merge iff the row
                                 lengths are skewed (max row > 16 d and >= 1024), there are too few
-                                rows to fill the row-split kernel (m < 2 x resident row groups), or
+                                rows to fill the row-split kernel (m < 2 x resident row groups, with
+                                nnz >= 2^20), or
                                 the rows are too long to stage a 16-row tile (1.2 x 16 d > 8192);
                                 costs one O(m) device reduction + stream sync at plan time.  */
     int32_t partition;       /* spmm_partition for the merge kernel: 2-D merge path over (row ends,

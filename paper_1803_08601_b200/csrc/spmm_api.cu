@@ -577,7 +577,9 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             const bool skewed = (double)hmax > 16.0 * d && hmax >= 1024;
             const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true);
             const long long groups = (long long)num_sms() * 2 * TE_CWARPS * (32 / rc.G);  // resident row groups
-            const bool few_rows = h->m < 2 * groups;
+            // (only when there is enough work for idle row groups to matter: a small matrix is
+            // launch-bound, and the single row-split launch beats merge's three -- config 0: 15 vs 51 us)
+            const bool few_rows = h->m < 2 * groups && h->nnz >= (1LL << 20);
             // rows so long that even a 16-row tile overflows the staged CSR slice: the row-split kernel
             // would stream A from global per row group (measured 2.5x slower than merge at d = 1000,
             // profiles/r01_density_sweep.txt), while merge path stages fixed-size slices at any d

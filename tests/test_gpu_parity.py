@@ -269,6 +269,15 @@ def test_heuristic_choice_matches_oracle_rule():
     op.close()
 
 
+def test_auto_few_rows_guard_needs_enough_work():
+    # few rows + large work (aspect 1024 x 16384) -> merge; few rows + tiny work (config 0) -> row split
+    for pat, want in ((synth.aspect(1 << 24, 1 << 10), "merge"), (synth.config_pattern(0), "rowsplit")):
+        vd = synth.values(pat.nnz, 1, "f32_plus_times").to(DEV)
+        op = S.CsrSpmm(pat.row_offsets.to(DEV), pat.col_indices.to(DEV), vd, pat.k)
+        assert op.plan(64, "auto") == want
+        op.close()
+
+
 def test_auto_picks_merge_for_rows_too_long_to_stage():
     # 1.2 x 16 x d > 8192 <=> d > 426: a 16-row tile no longer fits the staged slice
     for d, want in ((400, "rowsplit"), (450, "merge")):
