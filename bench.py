@@ -122,7 +122,7 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # workloads
 # ------------------------------------------------------------------------------------------------
-def build_local(cfg: int, rank: int, world: int, dev, part_mode: int):
+def build_local(cfg: int, rank: int, world: int, dev, part_mode: int, distributed: bool = False):
     """Local CSR block (device) + global k + scaling mode."""
     if cfg == 1:
         M = 1 << 20
@@ -132,7 +132,7 @@ def build_local(cfg: int, rank: int, world: int, dev, part_mode: int):
     if cfg == 0:
         return synth.config_pattern(0, device=dev), 1024, 0, "weak"
     full = synth.config_pattern(cfg, device=dev)
-    if world == 1:
+    if not distributed:
         return full, full.k, 0, "strong"
     from paper_1803_08601_b200 import dist
     bounds = dist.partition_rows(full.row_offsets.cpu(), world, part_mode)
@@ -264,6 +264,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     n = args.n
     workload = WORKLOADS[args.config]
+    # launched by torchrun (even with one rank): run the multi-GPU path -- NCCL process group, row-block
+    # partition, broadcast of B, max-over-ranks reductions, optional all-gather of C
+    distributed = world > 1 or "LOCAL_RANK" in os.environ
 
     if args.impl == "reference":
         return run_reference(args, world, rank, workload)
@@ -273,23 +276,23 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    if distributed:
         tdist.init_process_group("nccl", device_id=dev)
 
     def barrier():
-        if world > 1:
+        if distributed:
             tdist.barrier()
 
     kind = "f32_plus_times"
     seed = synth.STRUCT_SEED + args.config
-    p, kg, zoff, scaling = build_local(args.config, rank, world, dev, args.row_partition)
+    p, kg, zoff, scaling = build_local(args.config, rank, world, dev, args.row_partition, distributed)
     vals = synth.values(p.nnz, seed + 100, kind, device=dev, offset=zoff)
     # B: generated on rank 0, broadcast to all ranks (north_star: "B is replicated by an NCCL broadcast")
     B = torch.empty(kg, n, dtype=torch.float32, device=dev)
     if rank == 0:
         B.copy_(synth.dense(kg, n, seed + 200, kind, device=dev))
     bcast_ms = None
-    if world > 1:
+    if distributed:
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -346,7 +349,7 @@ def main():
     step_ms = [ev[0].elapsed_time(ev[-1]) for ev in evsets]
     dom_ms = [ev[dominant - 1].elapsed_time(ev[dominant]) for ev in evsets]
     tot = torch.tensor([sum(step_ms), sum(dom_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if distributed:
         tdist.all_reduce(tot, op=tdist.ReduceOp.MAX)
         agg = torch.tensor([flops_local, float(balg), float(p.nnz)], dtype=torch.float64, device=dev)
         tdist.all_reduce(agg)
@@ -369,7 +372,7 @@ def main():
 
     # optional all-gather of C, timed separately from the SpMM
     allgather_ms = None
-    if world > 1 and args.gather_c:
+    if distributed and args.gather_c:
         rows = torch.tensor([p.m], dtype=torch.int64, device=dev)
         allr = [torch.empty_like(rows) for _ in range(world)]
         tdist.all_gather(allr, rows)
@@ -402,7 +405,7 @@ def main():
     # ---------------- e2e: host buffers through the public API ----------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, p, vals, B, kg, n, world, rank, dev, sampler, flops_all, tdist if world > 1 else None)
+        e2e = run_e2e(args, p, vals, B, kg, n, world, rank, dev, sampler, flops_all, tdist if distributed else None)
     sampler.stop()
     clocks = sampler.summary()
 
@@ -445,7 +448,7 @@ def main():
         }
         print(json.dumps(out), flush=True)
     op.close()
-    if world > 1:
+    if distributed:
         tdist.destroy_process_group()
 
 

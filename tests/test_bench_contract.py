@@ -46,3 +46,30 @@ def test_cuda_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     assert d["config"]["algo"] == "rowsplit" and d["config"]["l2"].startswith("flushed")
     assert d["dtype"] == "f32" and d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["1", "2"])
+def test_torchrun_single_rank_exercises_the_distributed_path(cfg):
+    """Under torchrun (even one rank) bench.py runs the multi-GPU plumbing for real: NCCL process group,
+    row-block partition + slicing, broadcast of B (timed), max-over-ranks reductions, all-gather of C
+    (timed) and the e2e path with the broadcast."""
+    import socket
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "1", "--config", cfg, "--steps", "3", "--warmup", "3", "--gather-c",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    assert d["config"]["bcast_B_ms"] is not None and d["config"]["allgather_C_ms"] is not None
+    assert "NCCL broadcast" in d["e2e"]["includes"]
