@@ -435,7 +435,10 @@ def main():
                        "l2": "flushed before every timed step (2x L2 bytes written)" if not args.no_flush
                        else "not flushed",
                        "parallelism": f"row-block x{world}", "bcast_B_ms": bcast_ms, "allgather_C_ms": allgather_ms,
+                       "step_plus_collectives_ms": (round(ms_per_step + (bcast_ms or 0.0) + (allgather_ms or 0.0), 5)
+                                                    if (bcast_ms is not None or allgather_ms is not None) else None),
                        "mean_row_length": info["mean_row_length"], "max_row_length": info["max_row_length"]},
+            "ms_per_step_median_rank0": round(statistics.median(step_ms), 5), "ms_per_step_min_rank0": round(min(step_ms), 5),
             "hbm_gbs_alg": round(gbs, 1), "bytes_alg_per_step": int(balg_all),
             "frac_of_roofline_step": round(gbs / peak, 4),
             "warm_l2_ms_per_step": round(warm_ms, 5), "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
