@@ -45,8 +45,10 @@ struct NzPred {  // first r with ro[r] > t
 
 // states[2c] = row, states[2c+1] = nonzero, c in [0, num_ctas]
 __global__ void __launch_bounds__(THREADS)
-k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states) {
+k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states,
+            int* __restrict__ tile_ctr = nullptr) {
     const int lane = threadIdx.x & 31;
+    if (tile_ctr && blockIdx.x == 0 && threadIdx.x == 0) *tile_ctr = 0;  // compute kernel's tile queue
     const long long c = (long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
     if (c > num_ctas) return;
     long long row, nz;

@@ -54,6 +54,9 @@ constexpr int kNumSMs = 148;
 #ifndef MG_U
 #define MG_U 8
 #endif
+#ifndef MG_DYN
+#define MG_DYN 1  // merge: CTAs take tiles from a global queue (zeroed by k_partition), not a static round robin
+#endif
 #ifndef MG_FOLD
 #define MG_FOLD 0  // merge with lane-folded workers for n <= 16 (experimental; slower on B200 so far)
 #endif
@@ -365,12 +368,14 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     int* carry_flag = reinterpret_cast<int*>(ws + off);
     off += align256(sizeof(int) * NC);
     T* carry_val = reinterpret_cast<T*>(ws + off);
+    off += align256(sizeof(T) * (size_t)NC * h->n);
+    int* tile_ctr = MG_DYN ? reinterpret_cast<int*>(ws + off) : nullptr;
     const int items = h->items;
     // phase 1: PartitionSpmm (Alg. 1 line 2)
     const long long pgrid = (NC + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     mark(h, 0, st);
     k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, (int)h->m, (int)h->nnz, items, h->opts.partition, (int)NC,
-                                                     states);
+                                                     states, tile_ctr);
     mark(h, 1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -381,6 +386,7 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     P.carry_row = carry_row;
     P.carry_flag = carry_flag;
     P.carry_val = carry_val;
+    P.tile_ctr = tile_ctr;
     P.capr = items + 8;
     P.capz = items + 8;
     P.stages = std::max(2, std::min(TE_MAX_STAGES, (int)(MG_SMEM_BUDGET / te_buf_bytes(P.capr, P.capz, (int)sizeof(T)))));
@@ -596,7 +602,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         if (NC > 0) {
             const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
             h->ws_bytes = align256(sizeof(int) * 2 * (NC + 1)) + 2 * align256(sizeof(int) * NC) +
-                          align256(elem * (size_t)NC * n);
+                          align256(elem * (size_t)NC * n) + (MG_DYN ? 256 : 0);
         }
     } else {
         // row tiles of R rows sized so a typical tile's nonzeros fit the staged shared-memory slice

@@ -62,6 +62,7 @@ struct TileParams {
     unsigned pf_bytes;  // bytes of each B row to prefetch into L2 ahead of the consumers (0 = off)
     int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
     int capb;           // rowsplit: bytes per stage for the tile's B row span (0 = B is gathered from global)
+    int* tile_ctr;      // merge, MG_DYN: global tile queue (zeroed by k_partition); null = static round robin
 };
 
 // tile descriptor written by the producer next to the staged data
@@ -312,7 +313,17 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
         const bool bstage = MODE == MODE_ROWSPLIT && P.capb > 0;
         const bool val_tma = te_phase(P.col) == te_phase(P.val);
         int pend = -1;  // B staging: tile index whose CSR slice is in flight
-        for (int c = blockIdx.x; c < P.num_ranges; c += gridDim.x) {
+        // tiles: static round robin, or (merge with a tile queue) taken from a global counter so CTAs that
+        // finish early take more of the latency-variable tiles
+        auto next_tile = [&](int cur) -> int {
+            if (MODE == MODE_MERGE && P.tile_ctr) {
+                int nx = 0;
+                if (lane == 0) nx = atomicAdd(P.tile_ctr, 1);
+                return __shfl_sync(FULL, nx, 0);
+            }
+            return cur < 0 ? (int)blockIdx.x : cur + (int)gridDim.x;
+        };
+        for (int c = next_tile(-1); c < P.num_ranges; c = next_tile(c)) {
             long long rs, zs, re, ze;
             if (MODE == MODE_ROWSPLIT) {
                 rs = (long long)c * P.rows_per_tile;
