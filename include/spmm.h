@@ -131,7 +131,8 @@ SPMM_API spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int6
  * spmm_csr_plan -- choose the kernel for B with n columns (1 <= n <= 128) and size the workspace.
  *   algo_or_auto: force ROWSPLIT / MERGE, or AUTO (§5.4 heuristic).
  *   threshold <= 0 -> 9.35.  *workspace_bytes receives the device workspace size
- *   execute() needs (0 for row split); *chosen receives ROWSPLIT or MERGE.  Either out pointer may
+ *   execute() needs (row split: 0, or 256 bytes for its tile queue when AUTO finds irregular row lengths);
+ *   *chosen receives ROWSPLIT or MERGE.  Either out pointer may
  *   be NULL.  Plan enqueues small measurement kernels on `stream` and synchronises it: the maximum
  *   row length (AUTO policy) and, for the row-split kernel with n * 4 >= 256 bytes, the compactness
  *   of the row tiles' B spans (B staging, see spmm_plan_info.b_staging).  Plan once, execute often.

@@ -313,10 +313,10 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
         const bool bstage = MODE == MODE_ROWSPLIT && P.capb > 0;
         const bool val_tma = te_phase(P.col) == te_phase(P.val);
         int pend = -1;  // B staging: tile index whose CSR slice is in flight
-        // tiles: static round robin, or (merge with a tile queue) taken from a global counter so CTAs that
-        // finish early take more of the latency-variable tiles
+        // tiles: static round robin, or (merge; row split with irregular rows) taken from a global queue
+        // so CTAs that finish early take more of the variable-cost tiles
         auto next_tile = [&](int cur) -> int {
-            if (MODE == MODE_MERGE && P.tile_ctr) {
+            if (P.tile_ctr) {
                 int nx = 0;
                 if (lane == 0) nx = atomicAdd(P.tile_ctr, 1);
                 return __shfl_sync(FULL, nx, 0);

@@ -278,6 +278,21 @@ def test_auto_few_rows_guard_needs_enough_work():
         op.close()
 
 
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("n", [8, 64, 128])
+def test_rowsplit_tile_queue_for_irregular_rows(kind, n):
+    # lognormal rows (max row >> mean, but below the merge skew guard): AUTO keeps row split and takes
+    # the row tiles from a queue in the workspace (256 bytes); results unchanged
+    p = synth.lognormal_rows(20000, 9000, 7.92, 77)
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    chosen, info = run_gpu(p, kind, n, "auto", ro, ci, vd, Bd, Cd)
+    assert chosen == "rowsplit" and info["workspace_bytes"] == 256
+    check(p, kind, n, val, Bh, Cd)
+    # executing twice with the same workspace re-zeroes the queue
+    run_gpu(p, kind, n, "auto", ro, ci, vd, Bd, Cd)
+    check(p, kind, n, val, Bh, Cd)
+
+
 def test_auto_picks_merge_for_rows_too_long_to_stage():
     # 1.2 x 16 x d > 8192 <=> d > 426: a 16-row tile no longer fits the staged slice
     for d, want in ((400, "rowsplit"), (450, "merge")):
