@@ -451,6 +451,23 @@ cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, lo
 
 }  // namespace
 
+// plan-time O(m) device reduction: the longest row (AUTO policy guards, row-split tile queue)
+static spmm_status measure_max_row(spmm_csr_t h, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int hmax = 0;
+    cudaError_t e = cudaMemsetAsync(h->d_scratch, 0, sizeof(int), st);
+    if (e == cudaSuccess) {
+        const int grid = (int)std::min<long long>((h->m + THREADS - 1) / THREADS, 8LL * kNumSMs);
+        k_max_row<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->m, h->d_scratch);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hmax, h->d_scratch, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "plan: max row length");
+    h->max_row = hmax;
+    return SPMM_OK;
+}
+
 // ================================================================================================
 // C ABI
 // ================================================================================================
@@ -582,18 +599,9 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             // kernel handles short rows well, so the row-length threshold is replaced by the two causes of
             // Type 1 imbalance that merge path removes: a skewed row-length
             // distribution, or too few rows to fill the GPU's row groups.
-            cudaStream_t st = static_cast<cudaStream_t>(stream);
-            int hmax = 0;
-            cudaError_t e = cudaMemsetAsync(h->d_scratch, 0, sizeof(int), st);
-            if (e == cudaSuccess) {
-                const int grid = (int)std::min<long long>((h->m + THREADS - 1) / THREADS, 8LL * kNumSMs);
-                k_max_row<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->m, h->d_scratch);
-                e = cudaGetLastError();
-            }
-            if (e == cudaSuccess) e = cudaMemcpyAsync(&hmax, h->d_scratch, sizeof(int), cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return cuda_fail(h, e, "plan: max row length");
-            h->max_row = hmax;
+            const spmm_status ms = measure_max_row(h, stream);
+            if (ms != SPMM_OK) return ms;
+            const long long hmax = h->max_row;
             const bool skewed = (double)hmax > 16.0 * d && hmax >= 1024;
             const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true);
             const long long groups = (long long)num_sms() * 2 * TE_CWARPS * (32 / rc.G);  // resident row groups
@@ -675,7 +683,12 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         // irregular (but not merge-skewed) row lengths: uneven tile costs, so the persistent CTAs take
         // row tiles from a queue (measured: lognormal d = 7.9 -14%; regular matrices keep the static
         // round robin, which the queue's extra latency slows)
-        h->rs_dyn = h->max_row >= 0 && (double)h->max_row > RS_DYN_SKEW * std::max(1.0, d);
+        if (o.policy == SPMM_POLICY_AUTO && h->max_row < 0 && h->m > 0) {  // forced ROWSPLIT under AUTO policy
+            const spmm_status ms = measure_max_row(h, stream);
+            if (ms != SPMM_OK) return ms;
+        }
+        h->rs_dyn = o.policy == SPMM_POLICY_AUTO && h->max_row >= 0 &&
+                    (double)h->max_row > RS_DYN_SKEW * std::max(1.0, d);
         if (h->rs_dyn) h->ws_bytes = 256;
         if (o.row_pairing == SPMM_PAIRING_ON) {
             h->pairing = true;
