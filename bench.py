@@ -3,11 +3,13 @@
 
 One "step" = one C = A*B through spmm_csr_execute (the whole hot path of SURVEY.md §8(a): for the
 row-split choice one kernel, for merge: partition + compute + carry fix-up) over one synthetic input
-resident in HBM.  Default workload = BASELINE.json configs[1]: banded m = k = 2^20, 16 nnz/row,
-n = 64, fp32 (the AUTO heuristic picks row split there).  L2 is flushed (2x L2 bytes written) before
-every timed step.  Multi-GPU (torchrun): weak scaling on the banded family (global banded matrix of
-N*2^20 rows, rank r owns row block r, B broadcast from rank 0 over NCCL and timed separately), or
-strong scaling with nnz-balanced row blocks for the R-MAT configs.
+resident in HBM.  Default workload = BASELINE.json configs[4], the config the metric's multi-GPU
+target is quoted on: R-MAT scale 26 (Graph500 a,b,c,d = .57,.19,.19,.05, edge factor 16), n = 64,
+fp32, strong scaling -- on N GPUs (torchrun) A is split into merge-path balanced row blocks
+(dist.RowBlockSpmm: partition, slice, NCCL broadcast of B, local execute, optional all-gather of C --
+the same object the multi-GPU tests check against the oracle).  On one GPU (no torchrun) configs[1]
+(banded 2^20) and configs[2] (R-MAT 22) are measured in the same process as extra keys.  L2 is
+flushed (2x L2 bytes written) before every timed step.
 
 Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (oracle/, plain C) on a
 bounded sample of the same workload instead.
@@ -15,8 +17,8 @@ bounded sample of the same workload instead.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
-import math
 import os
 import statistics
 import sys
@@ -34,11 +36,13 @@ METRIC = "SpMM GFLOP/s and HBM GB/s (fraction of roofline) at n=64, 1/2/4/8 B200
 UNIT = "GFLOP/s"
 
 WORKLOADS = {
-    1: "banded m=k=2^20 (x N ranks, weak), 16 nnz/row, n=64, fp32 plus-times (BASELINE configs[1])",
+    4: "R-MAT scale 26, avg deg 16, n=64, fp32 plus-times, merge-path balanced row blocks, strong scaling "
+       "(BASELINE configs[4])",
     2: "R-MAT scale 22, avg deg 16, n=64, fp32 plus-times (BASELINE configs[2])",
-    4: "R-MAT scale 26, avg deg 16, n=64, fp32 plus-times, row blocks (BASELINE configs[4])",
+    1: "banded m=k=2^20 (x N ranks, weak), 16 nnz/row, n=64, fp32 plus-times (BASELINE configs[1])",
     0: "tiny uniform m=k=1024, 16 nnz/row, n=64, fp32 plus-times (BASELINE configs[0])",
 }
+KERNEL_NAMES = {"rowsplit": "k_tile<ROWSPLIT>", "merge": "k_merge_w"}
 
 
 def peaks():
@@ -61,7 +65,6 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 class ClockSampler:
     def __init__(self, device_index: int, interval: float = 0.002):
         self.samples = []
-        self.reasons = set()
         self.max_mhz = None
         self._stop = threading.Event()
         self._active = threading.Event()
@@ -91,8 +94,7 @@ class ClockSampler:
                         r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                     except Exception:
                         r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                    util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
-                    self.samples.append((mhz, r, util))
+                    self.samples.append((mhz, r))
                 except Exception:
                     pass
             time.sleep(self.interval)
@@ -111,7 +113,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"], "samples": 0}
         loaded = [s for s in self.samples if not (s[1] & 0x1)] or self.samples
         reasons = set()
-        for _, r, _ in loaded:
+        for _, r in loaded:
             for bit, name in REASONS.items():
                 if r & bit and bit != 0x1:
                     reasons.add(name)
@@ -120,105 +122,75 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-# workloads
+# workload bookkeeping
 # ------------------------------------------------------------------------------------------------
-def build_local(cfg: int, rank: int, world: int, dev, part_mode: int, distributed: bool = False):
-    """Local CSR block (device) + global k + scaling mode."""
-    if cfg == 1:
-        M = 1 << 20
-        mg = M * world
-        p = synth.banded(mg, device=dev, row_begin=rank * M, row_end=(rank + 1) * M)
-        return p, mg, rank * M * 16, "weak"
-    if cfg == 0:
-        return synth.config_pattern(0, device=dev), 1024, 0, "weak"
-    full = synth.config_pattern(cfg, device=dev)
-    if not distributed:
-        return full, full.k, 0, "strong"
-    from paper_1803_08601_b200 import dist
-    bounds = dist.partition_rows(full.row_offsets.cpu(), world, part_mode)
-    r0, r1 = bounds[rank], bounds[rank + 1]
-    ro = full.row_offsets[r0:r1 + 1]
-    z0, z1 = int(ro[0]), int(ro[-1])
-    p = synth.CsrPattern(r1 - r0, full.k, (ro - z0).contiguous(), full.col_indices[z0:z1].contiguous(), full.name)
-    return p, full.k, z0, "strong"
-
-
 def bytes_alg(p: synth.CsrPattern, n: int) -> int:
     """4(m+1) + 8 nnz + 4n |distinct cols| + 4n m (fp32/int32 values, int32 indices)."""
     distinct = int(torch.unique(p.col_indices).numel()) if p.nnz else 0
     return 4 * (p.m + 1) + 8 * p.nnz + 4 * n * distinct + 4 * n * p.m
 
 
-def load_traffic(workload_key: str):
+def static_l2_ceiling(p: synth.CsrPattern, n: int, l2_bytes: int, balg: int, peak_gbs: float) -> dict:
+    """Attainable-fraction ceiling from a cache model: an ideal static L2 that holds the hottest B
+    rows (as many as fit in the whole L2, l2_bytes / 4n) and nothing else.  Every B-row gather to a
+    row outside that set misses; every row is fetched at least once (compulsory).  CSR and C stream
+    once.  HBM bytes of the model = CSR + C + 4n (distinct + sum over cold rows of (uses - 1)); the
+    ceiling is bytes_alg / model bytes (an optimistic bound: real L2s also hold CSR/C lines and
+    replace by recency, not by frequency)."""
+    if p.nnz == 0:
+        return {"model": "static-hot-rows", "frac_ceiling": 1.0}
+    cnt = torch.bincount(p.col_indices.to(torch.int64), minlength=p.k)
+    used = cnt[cnt > 0]
+    hot = int(l2_bytes // (4 * n))
+    srt = torch.sort(used, descending=True).values
+    cold = srt[hot:]
+    miss_extra = int((cold - 1).sum().item()) if cold.numel() else 0
+    model = balg + 4 * n * miss_extra
+    hits = int(srt[:hot].sum().item()) - min(hot, srt.numel())
+    return {"model": "ideal static L2 holding the hottest B rows (l2 bytes / 4n rows)",
+            "l2_bytes": l2_bytes, "model_hbm_bytes": int(model),
+            "b_gather_hit_rate": round(hits / p.nnz, 4),
+            "frac_ceiling": round(balg / model, 4),
+            "t_ceiling_ms": round(model / (peak_gbs * 1e9) * 1e3, 4)}
+
+
+def lib_sha16() -> str | None:
+    from paper_1803_08601_b200 import spmm as S
+    path = os.environ.get("SPMM_LIB") or S.LIB_PATH
+    try:
+        with open(path, "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def load_traffic(key: str, sha: str | None):
+    """ncu DRAM bytes / L2 hit rate of the dominant kernel for this workload, from the committed
+    capture (profiles/ncu_traffic.json, written by scripts/ncu_summary.py) -- reported only with the
+    library hash it was captured from, so a stale capture is visible as such."""
     f = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(f) as fh:
-            return json.load(fh).get(workload_key)
+            ent = json.load(fh).get(key)
     except Exception:
         return None
-
-
-# ------------------------------------------------------------------------------------------------
-# oracle timing (cpu_baseline / --impl reference)
-# ------------------------------------------------------------------------------------------------
-def oracle_time_sample(p_cpu: synth.CsrPattern, val_cpu, B_cpu, n: int, budget_s: float):
-    """Time the oracle (as it stands, all host cores via OpenMP) on the workload: the first R rows
-    when the whole matrix would exceed budget_s, else the whole matrix repeated until about budget_s
-    of CPU time has elapsed.  Returns (gflops, seconds_per_run, rows, flops_per_run, runs)."""
-    import oracle
-    ro = p_cpu.row_offsets.numpy()
-    col = p_cpu.col_indices.numpy()
-    vals = val_cpu.numpy()
-    m = p_cpu.m
-
-    def run(R):
-        sub_ro = ro[:R + 1]
-        z = int(sub_ro[-1])
-        t0 = time.perf_counter()
-        oracle.spmm("f32_plus_times", R, p_cpu.k, n, sub_ro, col[:z], vals[:z], B_cpu, ldb=n)
-        return time.perf_counter() - t0, 2.0 * z * n
-
-    R = min(m, 4096)
-    dt, fl = run(R)
-    while dt < 0.05 * budget_s and R < m:
-        R = min(m, R * 4)
-        dt, fl = run(R)
-    if R < m:
-        R = min(m, max(1, int(R * budget_s / max(dt, 1e-6))))
-        dt, fl = run(R)
-    runs, tot = 1, dt
-    while tot < budget_s:  # whole workload fits the budget: repeat it
-        d2, _ = run(R)
-        tot += d2
-        runs += 1
-    return fl * runs / tot / 1e9, tot / runs, R, fl, runs
-
-
-def oracle_one_thread(p_cpu, val_cpu, B_np, n, budget_s):
-    """The oracle with OpenMP limited to one thread (restored afterwards); (GFLOP/s, rows) or None."""
-    import ctypes
-    import oracle
-    try:
-        gomp = ctypes.CDLL("libgomp.so.1")
-        prev = gomp.omp_get_max_threads()
-    except OSError:
+    if ent is None:
         return None
-    ro = p_cpu.row_offsets.numpy()
-    col = p_cpu.col_indices.numpy()
-    vals = val_cpu.numpy()
-    gomp.omp_set_num_threads(1)
+    if not isinstance(ent, dict):
+        ent = {"dram_bytes": ent}
+    ent = dict(ent)
+    ent["same_build"] = (ent.get("lib_sha16") == sha) if sha else None
+    return ent
+
+
+def physical_cores():
     try:
-        R = min(p_cpu.m, 2048)
-        while True:
-            z = int(ro[R])
-            t0 = time.perf_counter()
-            oracle.spmm("f32_plus_times", R, p_cpu.k, n, ro[:R + 1], col[:z], vals[:z], B_np, ldb=n)
-            dt = time.perf_counter() - t0
-            if dt > 0.25 * budget_s or R >= p_cpu.m:
-                return 2.0 * z * n / dt / 1e9, R
-            R = min(p_cpu.m, R * 4)
-    finally:
-        gomp.omp_set_num_threads(prev)
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = dict(line.split(":", 1) for line in out.splitlines() if ":" in line)
+        return int(kv["Core(s) per socket"].strip()) * int(kv.get("Socket(s)", "1").strip())
+    except Exception:
+        return None
 
 
 def cpu_model():
@@ -239,98 +211,83 @@ def cores():
 
 
 # ------------------------------------------------------------------------------------------------
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 4])
-    ap.add_argument("--n", type=int, default=64)
-    ap.add_argument("--algo", default="auto", choices=["auto", "rowsplit", "merge"])
-    ap.add_argument("--partition", default="merge_path", choices=["merge_path", "nonzero_split"])
-    ap.add_argument("--items", type=int, default=0)
-    ap.add_argument("--row-partition", type=int, default=1, help="multi-GPU: 0 nnz-balanced, 1 merge-path")
-    ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--gather-c", action="store_true", help="multi-GPU: also time an all-gather of C")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
-    args = ap.parse_args()
-    assert args.warmup >= 3 or args.impl == "reference", "timing rules: at least 3 warm-up steps"
+# oracle timing (cpu_baseline / --impl reference)
+# ------------------------------------------------------------------------------------------------
+def _prefix_cpu(p: synth.CsrPattern, vals, rows: int):
+    """The first `rows` rows of a (device) CSR and its values, on the host."""
+    ro = p.row_offsets[:rows + 1].cpu().numpy()
+    z = int(ro[-1])
+    return ro, p.col_indices[:z].cpu().numpy(), vals[:z].cpu().numpy()
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    n = args.n
-    workload = WORKLOADS[args.config]
-    # launched by torchrun (even with one rank): run the multi-GPU path -- NCCL process group, row-block
-    # partition, broadcast of B, max-over-ranks reductions, optional all-gather of C
-    distributed = world > 1 or "LOCAL_RANK" in os.environ
 
-    if args.impl == "reference":
-        return run_reference(args, world, rank, workload)
+def oracle_time_sample(p: synth.CsrPattern, vals, B_np, n: int, budget_s: float):
+    """Time the oracle (as it stands, all host cores via OpenMP) on a prefix of the workload's rows
+    sized to about budget_s; the whole matrix is repeated instead when it fits the budget.
+    Returns (gflops, seconds_per_run, rows, flops_per_run, runs)."""
+    import oracle
+    m = p.m
 
-    import torch.distributed as tdist
-    from paper_1803_08601_b200 import spmm as S
+    def run(R):
+        ro, col, v = _prefix_cpu(p, vals, R)
+        t0 = time.perf_counter()
+        oracle.spmm("f32_plus_times", R, p.k, n, ro, col, v, B_np, ldb=n)
+        return time.perf_counter() - t0, 2.0 * int(ro[-1]) * n
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    if distributed:
-        tdist.init_process_group("nccl", device_id=dev)
+    R = min(m, 4096)
+    dt, fl = run(R)
+    while dt < 0.05 * budget_s and R < m:
+        R = min(m, R * 4)
+        dt, fl = run(R)
+    if R < m:
+        R = min(m, max(1, int(R * budget_s / max(dt, 1e-6))))
+        dt, fl = run(R)
+    runs, tot = 1, dt
+    while tot < budget_s:  # whole workload fits the budget: repeat it
+        d2, _ = run(R)
+        tot += d2
+        runs += 1
+    return fl * runs / tot / 1e9, tot / runs, R, fl, runs
 
-    def barrier():
-        if distributed:
-            tdist.barrier()
 
-    kind = "f32_plus_times"
-    seed = synth.STRUCT_SEED + args.config
-    p, kg, zoff, scaling = build_local(args.config, rank, world, dev, args.row_partition, distributed)
-    vals = synth.values(p.nnz, seed + 100, kind, device=dev, offset=zoff)
-    # B: generated on rank 0, broadcast to all ranks (north_star: "B is replicated by an NCCL broadcast")
-    B = torch.empty(kg, n, dtype=torch.float32, device=dev)
-    if rank == 0:
-        B.copy_(synth.dense(kg, n, seed + 200, kind, device=dev))
-    bcast_ms = None
-    if distributed:
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        tdist.broadcast(B, src=0)
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        bcast_ms = float(t.item())
-    C = torch.empty(p.m, n, dtype=torch.float32, device=dev)
+def oracle_one_thread(p, vals, B_np, n, budget_s):
+    """The oracle with OpenMP limited to one thread (restored afterwards); (GFLOP/s, rows) or None."""
+    import ctypes
+    import oracle
+    try:
+        gomp = ctypes.CDLL("libgomp.so.1")
+        prev = gomp.omp_get_max_threads()
+    except OSError:
+        return None
+    gomp.omp_set_num_threads(1)
+    try:
+        R = min(p.m, 2048)
+        while True:
+            ro, col, v = _prefix_cpu(p, vals, R)
+            t0 = time.perf_counter()
+            oracle.spmm("f32_plus_times", R, p.k, n, ro, col, v, B_np, ldb=n)
+            dt = time.perf_counter() - t0
+            if dt > 0.25 * budget_s or R >= p.m:
+                return 2.0 * int(ro[-1]) * n / dt / 1e9, R
+            R = min(p.m, R * 4)
+    finally:
+        gomp.omp_set_num_threads(prev)
 
-    op = S.CsrSpmm(p.row_offsets, p.col_indices, vals, kg)
-    chosen = op.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items)
-    info = op.info()
+
+# ------------------------------------------------------------------------------------------------
+# device timing of one planned operator
+# ------------------------------------------------------------------------------------------------
+def time_steps(op_local, execute, steps: int, warmup: int, flush_buf, sampler, barrier, no_flush=False):
+    """W warm-up + K timed executes with per-kernel CUDA events recorded by the library on the execute
+    stream (spmm_csr_set_timing_events).  Returns (step_ms list, compute-kernel ms list)."""
+    info = op_local.info()
     nev = info["launches_per_execute"] + 1
-    dominant = 1 if chosen == "rowsplit" else 2  # index of the dominant kernel's end event
-    balg = bytes_alg(p, n)
-    flops_local = 2.0 * p.nnz * n
-
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush_buf = torch.empty(int(2 * l2) // 4 + 1024, dtype=torch.float32, device=dev)
-    sampler = ClockSampler(local_rank)
-
-    def step(events=None):
-        if events is not None:
-            op.set_timing_events(events)
-        op.execute(B, C)
-
-    # warm-up
-    for _ in range(args.warmup):
-        if not args.no_flush:
+    ci = info["compute_launch"]
+    for _ in range(warmup):
+        if not no_flush:
             flush_buf.zero_()
-        step()
+        execute()
     torch.cuda.synchronize()
-
-    # timed region: K steps, per-step CUDA events recorded by the library around each kernel
-    evsets = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
+    evsets = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(steps)]
     for evs in evsets:  # torch creates the CUDA event lazily on first record: force creation
         for e in evs:
             e.record()
@@ -338,138 +295,284 @@ def main():
     barrier()
     torch.cuda.synchronize()
     sampler.start()
-    for k in range(args.steps):
-        if not args.no_flush:
+    for k in range(steps):
+        if not no_flush:
             flush_buf.zero_()
-        step(evsets[k])
+        op_local.set_timing_events(evsets[k])
+        execute()
     torch.cuda.synchronize()
     sampler.pause()
     barrier()
-    op.set_timing_events([])
+    op_local.set_timing_events([])
     step_ms = [ev[0].elapsed_time(ev[-1]) for ev in evsets]
-    dom_ms = [ev[dominant - 1].elapsed_time(ev[dominant]) for ev in evsets]
-    tot = torch.tensor([sum(step_ms), sum(dom_ms)], dtype=torch.float64, device=dev)
+    dom_ms = [ev[ci].elapsed_time(ev[ci + 1]) for ev in evsets]
+    return step_ms, dom_ms
+
+
+def measure_single(cfg: int, n: int, args, dev, flush_buf, sampler, peak, l2_bytes, sha, with_ceiling=True):
+    """One GPU, no process group: plan + K timed executes of configs[cfg] through CsrSpmm."""
+    from paper_1803_08601_b200 import spmm as S
+    kind = "f32_plus_times"
+    seed = synth.STRUCT_SEED + cfg
+    p = synth.config_pattern(cfg, device=dev)
+    vals = synth.values(p.nnz, seed + 100, kind, device=dev)
+    B = synth.dense(p.k, n, seed + 200, kind, device=dev)
+    C = torch.empty(p.m, n, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    op = S.CsrSpmm(p.row_offsets, p.col_indices, vals, p.k)
+    chosen = op.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    info = op.info()
+    step_ms, dom_ms = time_steps(op, lambda: op.execute(B, C), args.steps, args.warmup, flush_buf, sampler,
+                                 lambda: None, args.no_flush)
+    balg = bytes_alg(p, n)
+    res = summarize(p, n, balg, chosen, info, step_ms, dom_ms, args.steps, peak, sha, cfg, plan_ms)
+    if with_ceiling:
+        res["roofline"]["ceiling"] = static_l2_ceiling(p, n, l2_bytes, balg, peak[0])
+    return res, (p, vals, B, C, op)
+
+
+def summarize(p, n, balg, chosen, info, step_ms, dom_ms, steps, peak, sha, cfg, plan_ms):
+    total_ms = sum(step_ms)
+    flops = 2.0 * p.nnz * n
+    dom_avg = sum(dom_ms) / len(dom_ms)
+    achieved = balg / (dom_avg / 1e3) / 1e9
+    kname = KERNEL_NAMES[chosen]
+    return {
+        "workload": WORKLOADS[cfg], "m": p.m, "k": p.k, "nnz": p.nnz, "n": n, "algo": chosen,
+        "mean_row_length": info["mean_row_length"], "max_row_length": info["max_row_length"],
+        "items_per_task": info["items_per_cta"] if chosen == "merge" else None,
+        "value": round(flops * steps / (total_ms / 1e3) / 1e9, 3), "unit": UNIT,
+        "ms_per_step": round(total_ms / steps, 5),
+        "ms_per_step_median": round(statistics.median(step_ms), 5), "ms_per_step_min": round(min(step_ms), 5),
+        "plan_ms": round(plan_ms, 3),
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak[0],
+                     "peak_source": peak[1], "unit": "GB/s", "frac": round(achieved / peak[0], 4),
+                     "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
+                     "traffic": None, "bytes_alg_per_launch": int(balg), "avg_launch_ms": round(dom_avg, 5),
+                     "ncu": load_traffic(f"config{cfg}_n{n}|{kname}", sha)},
+        "launches_per_step": info["launches_per_execute"],
+    }
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[0, 1, 2, 4])
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--algo", default="auto", choices=["auto", "rowsplit", "merge"])
+    ap.add_argument("--partition", default="merge_path", choices=["merge_path", "nonzero_split"])
+    ap.add_argument("--items", type=int, default=0)
+    ap.add_argument("--row-partition", type=int, default=1, help="multi-GPU: 0 nnz-balanced, 1 merge-path")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--gather-c", action="store_true", help="multi-GPU: also time the all-gather of C")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the configs[1]/[2] keys on one GPU")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "timing rules: at least 3 warm-up steps"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # launched by torchrun (even with one rank): the multi-GPU path -- NCCL process group, row-block
+    # partition, broadcast of B, max-over-ranks reductions, optional all-gather of C
+    distributed = world > 1 or "LOCAL_RANK" in os.environ
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch.distributed as tdist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     if distributed:
-        tdist.all_reduce(tot, op=tdist.ReduceOp.MAX)
-        agg = torch.tensor([flops_local, float(balg), float(p.nnz)], dtype=torch.float64, device=dev)
-        tdist.all_reduce(agg)
-        flops_all, balg_all, nnz_all = (float(x) for x in agg.tolist())
+        tdist.init_process_group("nccl", device_id=dev)
+    n = args.n
+    peak = peaks()
+    sha = lib_sha16()
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.empty(int(2 * l2) // 4 + 1024, dtype=torch.float32, device=dev)
+    sampler = ClockSampler(local_rank)
+
+    if distributed:
+        head, ctx = measure_distributed(args, world, rank, dev, flush_buf, sampler, peak, sha, l2)
     else:
-        flops_all, balg_all, nnz_all = flops_local, float(balg), float(p.nnz)
-    total_ms, dom_total_ms = float(tot[0]), float(tot[1])
-
-    # warm-L2 companion number (the cold, flushed figure is primary): same steps, no flush
-    warm_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(min(args.steps, 20))]
-    for evs in warm_sets:
-        for e in evs:
-            e.record()
-    torch.cuda.synchronize()
-    for evs in warm_sets:
-        step(evs)
-    torch.cuda.synchronize()
-    op.set_timing_events([])
-    warm_ms = sorted(ev[0].elapsed_time(ev[-1]) for ev in warm_sets)[len(warm_sets) // 2]
-
-    # optional all-gather of C, timed separately from the SpMM
-    allgather_ms = None
-    if distributed and args.gather_c:
-        rows = torch.tensor([p.m], dtype=torch.int64, device=dev)
-        allr = [torch.empty_like(rows) for _ in range(world)]
-        tdist.all_gather(allr, rows)
-        mx = max(int(r.item()) for r in allr)
-        pad = torch.zeros(mx, n, dtype=C.dtype, device=dev)
-        pad[:p.m] = C
-        parts = [torch.empty_like(pad) for _ in range(world)]
-        tdist.all_gather(parts, pad)  # warm-up
-        torch.cuda.synchronize()
-        barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record()
-        tdist.all_gather(parts, pad)
-        g1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([g0.elapsed_time(g1)], device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        allgather_ms = float(t.item())
-        del parts, pad
-    ms_per_step = total_ms / args.steps
-    value = flops_all * args.steps / (total_ms / 1e3) / 1e9
-    gbs = balg_all * args.steps / (total_ms / 1e3) / 1e9
-    peak, peak_src = peaks()
-    # roofline of the dominant kernel (this rank's algorithmic bytes / its average launch duration)
-    dom_avg_ms = sum(dom_ms) / len(dom_ms)
-    achieved = balg / (dom_avg_ms / 1e3) / 1e9
-    kernel_name = "k_tile<ROWSPLIT>" if chosen == "rowsplit" else "k_tile<MERGE>"
-    traffic = load_traffic(f"config{args.config}_n{n}|{kernel_name}") if world == 1 else None
+        head, ctx = measure_single(args.config, n, args, dev, flush_buf, sampler, peak, l2, sha)
+        head["scaling"] = "weak" if args.config in (0, 1) else "strong"
+        head["bcast_B_ms"] = head["allgather_C_ms"] = None
+        head["flops_all"] = 2.0 * head["nnz"] * n
+        head["ms_max"] = head["ms_per_step"]
 
     # ---------------- e2e: host buffers through the public API ----------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, p, vals, B, kg, n, world, rank, dev, sampler, flops_all, tdist if distributed else None)
+        e2e = run_e2e(args, ctx, n, world, rank, dev, sampler, head["flops_all"], distributed)
+    # ---------------- extra configs in the same process (one GPU) ----------------
+    extras = {}
+    if not distributed and not args.no_extras:
+        del ctx
+        torch.cuda.empty_cache()
+        for cfg in (1, 2):
+            if cfg == args.config:
+                continue
+            r, c2 = measure_single(cfg, n, args, dev, flush_buf, sampler, peak, l2, sha)
+            c2[4].close()
+            del c2
+            torch.cuda.empty_cache()
+            extras[f"config{cfg}"] = r
     sampler.stop()
     clocks = sampler.summary()
 
     # ---------------- cpu baseline (rank 0, N=1) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        p_cpu = p.to("cpu")
-        gfl, dt, R, fl, runs = oracle_time_sample(p_cpu, vals.cpu(), B.cpu().numpy(), n, args.cpu_budget)
-        cpu = {"value": round(gfl, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
-               "sample": f"oracle (plain C, fp64 accumulation + |A||B| bound, OpenMP) on the first {R} of {p.m} "
-                         f"rows of the same workload ({fl / 2 / n:.0f} nnz) x {runs} runs, {dt:.3f} s per run"}
-        # the oracle at 1 thread too (a smaller sample of the same rows)
-        g1 = oracle_one_thread(p_cpu, vals.cpu(), B.cpu().numpy(), n, budget_s=4.0)
-        if g1 is not None:
-            cpu["value_1thread"] = round(g1[0], 4)
-            cpu["sample_1thread"] = f"first {g1[1]} rows, 1 OpenMP thread"
-            cpu["cpu_model"] = cpu_model()
+        cpu = cpu_baseline(args.config, n, dev, args.cpu_budget)
 
     if rank == 0:
+        roof = head["roofline"]
         out = {
-            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload, "n": n, "m_local": p.m, "k": kg, "nnz_total": int(nnz_all),
-                       "algo": chosen, "policy": "auto" if args.algo == "auto" else "forced",
-                       "partition": args.partition if chosen == "merge" else None,
+            "metric": METRIC, "value": head["value_all"] if distributed else head["value"], "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": head["ms_max"], "higher_is_better": True, "scaling": head["scaling"],
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": head["workload"], "n": n, "m": head["m"], "k": head["k"], "nnz_total": head["nnz"],
+                       "algo": head["algo"], "policy": "auto" if args.algo == "auto" else "forced",
+                       "partition": args.partition if head["algo"] == "merge" else None,
+                       "items_per_task": head["items_per_task"],
                        "l2": "flushed before every timed step (2x L2 bytes written)" if not args.no_flush
                        else "not flushed",
-                       "parallelism": f"row-block x{world}", "bcast_B_ms": bcast_ms, "allgather_C_ms": allgather_ms,
-                       "step_plus_collectives_ms": (round(ms_per_step + (bcast_ms or 0.0) + (allgather_ms or 0.0), 5)
-                                                    if (bcast_ms is not None or allgather_ms is not None) else None),
-                       "mean_row_length": info["mean_row_length"], "max_row_length": info["max_row_length"]},
-            "ms_per_step_median_rank0": round(statistics.median(step_ms), 5), "ms_per_step_min_rank0": round(min(step_ms), 5),
-            "hbm_gbs_alg": round(gbs, 1), "bytes_alg_per_step": int(balg_all),
-            "frac_of_roofline_step": round(gbs / peak, 4),
-            "warm_l2_ms_per_step": round(warm_ms, 5), "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
-            "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": round(achieved, 1), "peak": peak,
-                         "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "bytes_alg_per_launch": balg,
-                         "avg_launch_ms": round(dom_avg_ms, 5)},
-            "e2e": e2e, "gpu_launches": info["launches_per_execute"] * args.steps,
-            "clocks": clocks, "cpu_baseline": cpu,
+                       "parallelism": f"row-block x{world}",
+                       "row_partition": ("merge-path balanced" if args.row_partition == 1 else "nnz-balanced")
+                       if distributed else None,
+                       "bcast_B_ms": head["bcast_B_ms"], "allgather_C_ms": head["allgather_C_ms"],
+                       "mean_row_length": head["mean_row_length"], "max_row_length": head["max_row_length"]},
+            "ms_per_step_median_rank0": head["ms_per_step_median"], "ms_per_step_min_rank0": head["ms_per_step_min"],
+            "plan_ms": head["plan_ms"],
+            "roofline": roof,
+            "e2e": e2e, "gpu_launches": head["launches_per_step"] * args.steps,
+            "clocks": clocks, "cpu_baseline": cpu, "lib_sha16": sha,
         }
+        for key, r in extras.items():
+            out[key] = r
         print(json.dumps(out), flush=True)
-    op.close()
     if distributed:
         tdist.destroy_process_group()
 
 
-def run_e2e(args, p, vals, B, kg, n, world, rank, dev, sampler, flops_all, tdist):
+def measure_distributed(args, world, rank, dev, flush_buf, sampler, peak, sha, l2):
+    """torchrun: dist.RowBlockSpmm (the shipped multi-GPU path).  Config 1 is weak scaling (rank r
+    generates banded block r of an N*2^20-row matrix), the R-MAT configs strong scaling over
+    merge-path (or nnz) balanced row blocks of the whole matrix."""
+    import torch.distributed as tdist
+    from paper_1803_08601_b200 import dist as D
+    n = args.n
+    kind = "f32_plus_times"
+    seed = synth.STRUCT_SEED + args.config
+    if args.config == 1:
+        M = 1 << 20
+        kg = M * world
+        p = synth.banded(kg, device=dev, row_begin=rank * M, row_end=(rank + 1) * M)
+        vals = synth.values(p.nnz, seed + 100, kind, device=dev, offset=rank * M * 16)
+        scaling = "weak"
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op = D.RowBlockSpmm(p.row_offsets, p.col_indices, vals, kg, local=True, device=dev)
+    else:
+        full = synth.config_pattern(args.config, device=dev)
+        fvals = synth.values(full.nnz, seed + 100, kind, device=dev)
+        kg = full.k
+        scaling = "strong"
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op = D.RowBlockSpmm(full.row_offsets, full.col_indices, fvals, kg, mode=args.row_partition, device=dev)
+        r0, r1 = op.bounds[rank], op.bounds[rank + 1]
+        p = synth.CsrPattern(r1 - r0, kg, op.ro, op.col, full.name)
+        vals = op.val
+        del full, fvals
+    chosen = op.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items)
+    torch.cuda.synchronize()
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    info = op.info()
+    # exchange step 1: B generated on rank 0, NCCL broadcast (timed separately, max over ranks)
+    B = torch.empty(kg, n, dtype=torch.float32, device=dev)
+    if rank == 0:
+        B.copy_(synth.dense(kg, n, seed + 200, kind, device=dev))
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    op.broadcast_B(out=B)
+    e1.record()
+    torch.cuda.synchronize()
+    bcast_ms = _max_over_ranks(e0.elapsed_time(e1), dev)
+    C = torch.empty(op.m_local, n, dtype=torch.float32, device=dev)
+    step_ms, dom_ms = time_steps(op.local.op, lambda: op.execute(B, C), args.steps, args.warmup, flush_buf,
+                                 sampler, tdist.barrier, args.no_flush)
+    balg = bytes_alg(p, n)
+    res = summarize(p, n, balg, chosen, info, step_ms, dom_ms, args.steps, peak, sha, args.config, plan_ms)
+    tot = torch.tensor([sum(step_ms), float(p.nnz), float(balg)], dtype=torch.float64, device=dev)
+    mx = tot.clone()
+    tdist.all_reduce(mx, op=tdist.ReduceOp.MAX)
+    tdist.all_reduce(tot)
+    res["ms_max"] = round(float(mx[0]) / args.steps, 5)
+    res["flops_all"] = 2.0 * float(tot[1]) * n
+    res["value_all"] = round(res["flops_all"] * args.steps / (float(mx[0]) / 1e3) / 1e9, 3)
+    res["nnz"] = int(tot[1])
+    res["m"] = op.m
+    res["bytes_alg_all"] = int(tot[2])
+    res["roofline"]["rank"] = rank
+    res["scaling"] = scaling
+    res["bcast_B_ms"] = round(bcast_ms, 4)
+    # exchange step 2 (optional): the C gather (grouped broadcasts of the uneven row blocks)
+    res["allgather_C_ms"] = None
+    if args.gather_c:
+        Cfull = torch.empty(op.m, n, dtype=torch.float32, device=dev)
+        op.gather_C(C, Cfull)
+        torch.cuda.synchronize()
+        tdist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        op.gather_C(C, Cfull)
+        g1.record()
+        torch.cuda.synchronize()
+        res["allgather_C_ms"] = round(_max_over_ranks(g0.elapsed_time(g1), dev), 4)
+        del Cfull
+    return res, (p, vals, B, C, op)
+
+
+def _max_over_ranks(x: float, dev) -> float:
+    import torch.distributed as tdist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_e2e(args, ctx, n, world, rank, dev, sampler, flops_all, distributed):
     """Same metric through the public API with HOST (pinned) buffers: every step copies the step's
-    inputs (CSR block + B) host->device, creates + plans + executes, and reads C back."""
+    inputs (this rank's CSR block + B on rank 0) host->device, (broadcasts B,) creates + plans +
+    executes, and reads this rank's C rows back."""
     from paper_1803_08601_b200 import spmm as S
+    p, vals, B, C, op = ctx
+    kg = p.k
     ro_h = p.row_offsets.cpu().pin_memory()
     col_h = p.col_indices.cpu().pin_memory()
     val_h = vals.cpu().pin_memory()
     B_h = B.cpu().pin_memory() if rank == 0 else None
     C_h = torch.empty(p.m, n, dtype=torch.float32).pin_memory()
     ro_d, col_d, val_d = torch.empty_like(p.row_offsets), torch.empty_like(p.col_indices), torch.empty_like(vals)
-    B_d = torch.empty_like(B)
-    C_d = torch.empty(p.m, n, dtype=torch.float32, device=dev)
+    B_d = B  # reuse the device allocation (its contents are overwritten by the H2D copy / broadcast)
+    C_d = C
     h2d = ro_h.numel() * 4 + col_h.numel() * 4 + val_h.numel() * 4 + (B_h.numel() * 4 if B_h is not None else 0)
     d2h = C_h.numel() * 4
-    steps = max(3, min(args.steps, 10))
+    import torch.distributed as tdist
 
     def one():
         ro_d.copy_(ro_h, non_blocking=True)
@@ -477,18 +580,19 @@ def run_e2e(args, p, vals, B, kg, n, world, rank, dev, sampler, flops_all, tdist
         val_d.copy_(val_h, non_blocking=True)
         if B_h is not None:
             B_d.copy_(B_h, non_blocking=True)
-        if tdist is not None:
+        if distributed:
             tdist.broadcast(B_d, src=0)
-        op = S.CsrSpmm(ro_d, col_d, val_d, kg)
-        op.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items)
-        op.execute(B_d, C_d)
+        o = S.CsrSpmm(ro_d, col_d, val_d, kg)
+        o.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items)
+        o.execute(B_d, C_d)
         C_h.copy_(C_d, non_blocking=True)
-        op.close()
+        o.close()
 
     one()
     torch.cuda.synchronize()
-    if tdist is not None:
+    if distributed:
         tdist.barrier()
+    steps = max(1, args.e2e_steps)
     sampler.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -497,39 +601,53 @@ def run_e2e(args, p, vals, B, kg, n, world, rank, dev, sampler, flops_all, tdist
     e1.record()
     torch.cuda.synchronize()
     sampler.pause()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if tdist is not None:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms = float(t.item()) / steps
+    ms = e0.elapsed_time(e1)
+    if distributed:
+        ms = _max_over_ranks(ms, dev)
+    ms /= steps
     return {"value": round(flops_all / (ms / 1e3) / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 4), "steps": steps,
-            "includes": "H2D(CSR block, B) + create + plan + execute + D2H(C) per step" +
-                        (" + NCCL broadcast of B" if tdist is not None else "")}
+            "includes": "H2D(CSR block, B) + create + plan + execute + D2H(C block) per step" +
+                        (" + NCCL broadcast of B" if distributed else "")}
 
 
-def run_reference(args, world, rank, workload):
-    """--impl reference: the oracle (plain C, oracle/) as it stands, on the host cores, rank 0 only."""
+def cpu_baseline(cfg, n, dev, budget):
+    """The oracle on the GPU box's host cores, on a prefix of the same workload's rows."""
+    kind = "f32_plus_times"
+    seed = synth.STRUCT_SEED + cfg
+    p = synth.config_pattern(cfg, device=dev)
+    vals = synth.values(p.nnz, seed + 100, kind, device=dev)
+    B_np = synth.dense(p.k, n, seed + 200, kind, device=dev).cpu().numpy()
+    gfl, dt, R, fl, runs = oracle_time_sample(p, vals, B_np, n, budget)
+    cpu = {"value": round(gfl, 4), "unit": UNIT, "cores": cores(), "physical_cores": physical_cores(),
+           "kind": "oracle", "cpu_model": cpu_model(),
+           "sample": f"oracle (plain C, fp64 accumulation + |A||B| bound, OpenMP) on the first {R} of {p.m} "
+                     f"rows of the same workload ({fl / 2 / n:.0f} nnz) x {runs} runs, {dt:.3f} s per run"}
+    g1 = oracle_one_thread(p, vals, B_np, n, budget_s=4.0)
+    if g1 is not None:
+        cpu["value_1thread"] = round(g1[0], 4)
+        cpu["sample_1thread"] = f"first {g1[1]} rows, 1 OpenMP thread"
+    return cpu
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle (plain C, oracle/) as it stands, on the host cores, rank 0 only,
+    each step a bounded prefix of the same workload's rows."""
     if rank != 0:
         return
     n = args.n
     kind = "f32_plus_times"
     seed = synth.STRUCT_SEED + args.config
-    if args.config == 1:
-        p = synth.banded(1 << 20)
-    else:
-        p = synth.config_pattern(args.config, device="cuda" if torch.cuda.is_available() else "cpu").to("cpu")
-    vals = synth.values(p.nnz, seed + 100, kind)
-    B = synth.dense(p.k, n, seed + 200, kind).numpy()
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    p = synth.config_pattern(args.config, device=dev)
+    vals = synth.values(p.nnz, seed + 100, kind, device=dev)
+    B = synth.dense(p.k, n, seed + 200, kind, device=dev).cpu().numpy()
     total_budget = 150.0
     per_step = max(0.5, min(15.0, total_budget / max(1, args.steps + args.warmup)))
     gfl, dt, R, fl, _ = oracle_time_sample(p, vals, B, n, per_step)
-    # warm-up + K steps on that sample
-    import numpy as np
     import oracle
-    ro = p.row_offsets.numpy()[:R + 1]
+    ro, col, v = _prefix_cpu(p, vals, R)
     z = int(ro[-1])
-    col = p.col_indices.numpy()[:z]
-    v = vals.numpy()[:z]
     for _ in range(args.warmup):
         oracle.spmm(kind, R, p.k, n, ro, col, v, B, ldb=n)
     ts = []
@@ -545,9 +663,10 @@ def run_reference(args, world, rank, workload):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
            "higher_is_better": True, "scaling": "weak" if args.config in (0, 1) else "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": workload, "n": n},
-           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
-                            "sample": sample},
+           "config": {"workload": WORKLOADS[args.config], "n": n, "m": p.m, "k": p.k, "nnz_total": p.nnz,
+                      "sample_rows": R, "sample_nnz": z},
+           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(),
+                            "physical_cores": physical_cores(), "kind": "oracle", "sample": sample},
            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

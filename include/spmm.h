@@ -41,7 +41,10 @@
 extern "C" {
 #endif
 
-#define SPMM_ABI_VERSION 2
+/* ABI history: 2 = round 1; 3 = row pairing removed (the plan option field is reserved), merge
+ * items are per warp task, spmm_plan_info.compute_launch added, row split under the AUTO policy may
+ * need a 256-byte workspace (tile queue) -- callers must size the workspace from plan(). */
+#define SPMM_ABI_VERSION 3
 
 typedef struct spmm_csr_s* spmm_csr_t;
 
@@ -63,7 +66,6 @@ enum { SPMM_FLAG_VALIDATE = 1u };                                       /* one c
 
 typedef enum { SPMM_POLICY_AUTO = 0, SPMM_POLICY_PAPER = 1 } spmm_policy;
 typedef enum { SPMM_PARTITION_MERGE_PATH = 0, SPMM_PARTITION_NONZERO_SPLIT = 1 } spmm_partition;
-typedef enum { SPMM_PAIRING_AUTO = 0, SPMM_PAIRING_OFF = 1, SPMM_PAIRING_ON = 2 } spmm_row_pairing;
 
 /* Optional planner knobs (spmm_csr_plan_ex).  Zero-initialised = defaults. */
 typedef struct {
@@ -77,14 +79,10 @@ typedef struct {
     int32_t partition;       /* spmm_partition for the merge kernel: 2-D merge path over (row ends,
                                 nonzeros) (default) or the paper's 1-D nonzero split
                                 (PAPER.md:80, :89).                                                  */
-    int32_t items_per_cta;   /* merge-path items (rows + nonzeros) per CTA; 0 = default (2048).
-                                Must be a multiple of 256 in [256, 4096].                           */
-    int32_t row_pairing;     /* spmm_row_pairing for the row-split kernel (B200 extension):
-                                AUTO (0) = measure at plan time (one O(nnz) device pass + stream sync)
-                                how many B-row gathers pairing adjacent rows would share and pair
-                                when >= 25% of the nonzeros share (never under policy PAPER); OFF (1) =
-                                one row per lane group, the paper's row split; ON (2)
-                                = always pair.  The result is C = AB either way.                     */
+    int32_t items_per_cta;   /* merge-path items (rows + nonzeros) per merge task, the partition
+                                granularity of Alg. 1 line 2; 0 = sized at plan time (256..2048, about
+                                16 tasks per resident worker).  Must be a multiple of 32 in [32, 8192]. */
+    int32_t reserved0;       /* must be zero */
     int32_t reserved[4];     /* must be zero */
 } spmm_plan_opts;
 
@@ -97,10 +95,11 @@ typedef struct {
     double mean_row_length;  /* d = nnz/m */
     int64_t max_row_length;  /* -1 unless computed (AUTO policy) */
     double threshold;
-    int32_t num_ctas;        /* CTAs of the compute kernel */
-    int32_t items_per_cta;   /* merge only */
-    int32_t launches_per_execute;  /* kernels one execute() enqueues (row split 1, merge 3) */
-    int32_t row_pairing;     /* 1 if the row-split kernel runs on row pairs (see spmm_plan_opts) */
+    int32_t num_ctas;        /* row split: row tiles; merge: merge-path tasks */
+    int32_t items_per_cta;   /* merge only: items per task */
+    int32_t launches_per_execute;  /* operations one execute() enqueues: merge 3 (partition, compute,
+                                      fix-up); row split 1, or 2 when its tile queue is reset first */
+    int32_t compute_launch;  /* 0-based index of the compute kernel among them (timing events i..i+1) */
     size_t workspace_bytes;
     int32_t b_staging;       /* 1 if the row-split kernel stages compact B row spans in shared memory
                                 (TMA); measured at plan time, applied per tile at execute when B and

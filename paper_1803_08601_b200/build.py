@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspmm.so")
 SOURCES = [os.path.join(CSRC, "spmm_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "ptx.cuh", "tile.cuh", "merge.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "ptx.cuh", "tile.cuh", "merge.cuh", "merge_w.cuh")] + \
     [os.path.join(ROOT, "include", "spmm.h")]
 
 NVCC_FLAGS = [

@@ -66,12 +66,6 @@ __device__ __forceinline__ int ld_stream(const int* p) {
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ unsigned ld_stream_u(const void* p) {
-    unsigned v;
-    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
 // gather VEC consecutive elements of a B row (VEC in {1,2,4}); p must be VEC*4-byte aligned
 template <int VEC> __device__ __forceinline__ void ldg_vec(unsigned (&o)[VEC], const void* p);
 template <> __device__ __forceinline__ void ldg_vec<1>(unsigned (&o)[1], const void* p) {

@@ -1,25 +1,16 @@
 // merge.cuh -- Algorithm II, merge-based SpMM (§4.2, Algorithm 1), sm_100a.
 //
 // Phase 1, PartitionSpmm (Alg. 1 line 2): k_partition writes the merge-path state
-//   (row, nonzero) at which every CTA starts.  2-D merge path (Fig. 2(c)): CTA c starts on
-//   diagonal c*I of the merge of row-end offsets with nonzero indices (rows first on ties), so every
-//   CTA gets I items = rows + nonzeros, which also charges the C write of empty rows.
-//   1-D nonzero split (PAPER.md:80, the paper's own choice, :89): CTA c starts at nonzero c*I in the
-//   largest row r with ro[r] <= c*I.  One warp per boundary, 32-ary search (~6 dependent probes).
-// Phase 2 (Alg. 1 lines 3-23): k_merge.  Per CTA:
-//   GlobalToShared (line 5): the CTA's row-end slice and its (col, val) slice are staged into shared
-//     memory with coalesced 16-byte loads.
-//   Each warp is a "worker": it finds its own equal share of the CTA's items with a second merge-path
-//     search in shared memory, then streams them: (col, val) are read from shared memory as warp
-//     broadcasts (the paper's 32 `Broadcast` rounds, lines 14-17, without registers new_ind/new_val),
-//     U B-row gathers are issued back to back (lanes over columns, float4/float2, line 18), and each
-//     row-end item flushes the running row into C (identity for empty rows).  Because every lane of a
-//     worker sees the same row id, the paper's valB[32] + PrepareSpmm (CSR->COO, line 21) +
-//     ReduceToGlobalSpmm segmented reduction (line 22) collapse into a running accumulator that is
-//     written on each row end; this removes the T = 1 register limit.
-//   Carry-outs (line 22): a worker whose range ends inside a row keeps its partial;
-//     partials whose row is finished inside the same CTA are added into C by warp 0 after a CTA
-//     barrier (ascending worker order); the CTA's final open row becomes the CTA's carry-out.
+//   (row, nonzero) at which every task starts (the paper partitions per CTA; here a task is one merge
+//   worker's slice).  2-D merge path (Fig. 2(c)): task c starts on diagonal c*I of the
+//   merge of row-end offsets with nonzero indices (rows first on ties), so every task gets I items =
+//   rows + nonzeros, which also charges the C write of empty rows.  1-D nonzero split
+//   (PAPER.md:80, the paper's own choice, :89): task c starts at nonzero c*I in the largest row r with
+//   ro[r] <= c*I.  One warp per boundary, 32-ary search (~6 dependent probes).
+// Phase 2 (Alg. 1 lines 3-23) is k_merge_w in merge_w.cuh: each warp streams its tasks' items from
+//   global memory through small windows (the GlobalToShared of line 5 becomes a per-warp cp.async
+//   window), with a running accumulator flushed on each row end; a task's open row becomes its
+//   carry-out (line 22).
 // Phase 3, FixCarryOut (Alg. 1 line 24): k_fixup adds each run of consecutive CTA
 //   carry-outs that share a row into C[row], in ascending CTA order (deterministic, no atomics).
 // Ownership (SURVEY.md §8(c) ambiguity 20): the worker that consumes a row's end item writes the row;
@@ -45,10 +36,8 @@ struct NzPred {  // first r with ro[r] > t
 
 // states[2c] = row, states[2c+1] = nonzero, c in [0, num_ctas]
 __global__ void __launch_bounds__(THREADS)
-k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states,
-            int* __restrict__ tile_ctr = nullptr) {
+k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states) {
     const int lane = threadIdx.x & 31;
-    if (tile_ctr && blockIdx.x == 0 && threadIdx.x == 0) *tile_ctr = 0;  // compute kernel's tile queue
     const long long c = (long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
     if (c > num_ctas) return;
     long long row, nz;
@@ -74,8 +63,8 @@ k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int
     }
 }
 
-// FixCarryOut (Alg. 1 line 24): one warp per CTA carry; the first CTA of each run of equal carry
-// rows sums the run in ascending CTA order and adds it into C[row].
+// FixCarryOut (Alg. 1 line 24): one warp per task carry; the first task of each run of equal carry
+// rows sums the run in ascending task order and adds it into C[row].
 template <typename T, int SR>
 __global__ void __launch_bounds__(THREADS)
 k_fixup(int num_ctas, int n, const int* __restrict__ carry_row, const int* __restrict__ carry_flag,

@@ -60,11 +60,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
-// per-lane L2 prefetch of the line holding p (no register destination)
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 // TMA bulk prefetch of a contiguous global range into L2 (no shared-memory destination)
 __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -82,19 +77,7 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 
-// named barrier among `nthreads` threads (id 1..15; id 0 is __syncthreads)
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// predicated shared-memory load (no branch); o unchanged/undefined when !pred
-// shared-memory atomic add with acquire-release semantics at CTA scope; returns the old value
-__device__ __forceinline__ int smem_atom_add_acq_rel(int* p, int v) {
-    int old;
-    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
-    return old;
-}
-
+// predicated shared-memory load (no branch); 0 when !pred
 __device__ __forceinline__ unsigned lds_pred(uint32_t saddr, bool pred) {
     unsigned v;
     asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; mov.b32 %0, 0; @q ld.shared.b32 %0, [%1];}"
@@ -104,6 +87,11 @@ __device__ __forceinline__ unsigned lds_pred(uint32_t saddr, bool pred) {
 __device__ __forceinline__ unsigned lds_u32(uint32_t saddr) {
     unsigned v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(saddr));
+    return v;
+}
+__device__ __forceinline__ uint2 lds_u64(uint32_t saddr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(saddr));
     return v;
 }
 __device__ __forceinline__ uint4 lds_u128(uint32_t saddr) {
@@ -126,14 +114,6 @@ __device__ __forceinline__ const char* opaque_ptr(const char* p) {
     return q;
 }
 
-// Ampere-style async copy global -> shared (LDGSTS), 4/8/16 bytes, tracked per thread in groups
-template <int BYTES> __device__ __forceinline__ void cp_async(uint32_t dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(BYTES) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 template <int VEC> __device__ __forceinline__ void lds_vec(unsigned (&o)[VEC], uint32_t saddr);
 template <> __device__ __forceinline__ void lds_vec<1>(unsigned (&o)[1], uint32_t a) {
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(o[0]) : "r"(a));

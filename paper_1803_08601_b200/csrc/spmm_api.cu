@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -13,6 +14,7 @@
 #include "common.cuh"
 #include "merge.cuh"
 #include "tile.cuh"
+#include "merge_w.cuh"
 
 using namespace spmm;
 
@@ -38,8 +40,6 @@ struct spmm_csr_s {
     bool rs_dyn = false;          // row split: tiles from a queue in the workspace (irregular row lengths)
     double bspan_compact = -1.0;  // fraction of nonzeros in row tiles whose B span is compact (plan-time)
     size_t ws_bytes = 0;
-    bool pairing = false;      // row split on row pairs (spmm_plan_opts.row_pairing)
-    double pair_shared = -1.0; // fraction of nonzeros whose B row a pair shares (plan-time measurement)
     int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
     int32_t nev = 0;
@@ -52,24 +52,11 @@ constexpr int kNumSMs = 148;
 #ifndef RS_U
 #define RS_U 8
 #endif
-#ifndef MG_U
-#define MG_U 8
-#endif
 #ifndef RS_DYN_SKEW
 #define RS_DYN_SKEW 4.0  // row split takes tiles from a queue when (AUTO) max row > RS_DYN_SKEW x mean row
 #endif
-#ifndef MG_DYN
-#define MG_DYN 1  // merge: CTAs take tiles from a global queue (zeroed by k_partition), not a static round robin
-#endif
-#ifndef MG_FOLD
-#define MG_FOLD 0  // merge with lane-folded workers for n <= 16 (experimental; slower on B200 so far)
-#endif
 #ifndef RS_GDIV
 #define RS_GDIV 2  // row split, 16..32 vector lanes per row: split the row over lanes/RS_GDIV lanes
-#endif
-#ifndef TE_CARVE
-#define TE_CARVE 0  // 1: request the minimal shared-memory carveout (maximal L1); measured neutral to slower
-                    // (the SM re-partitions when the next kernel wants another split)
 #endif
 #ifndef RS_STAGES
 #define RS_STAGES 3
@@ -83,19 +70,23 @@ constexpr int kNumSMs = 148;
 #ifndef RS_ZF
 #define RS_ZF 12  // row split: staged capacity = RS_ZF/10 x the tile's expected nonzeros
 #endif
-#ifndef MG_SMEM_BUDGET
-#define MG_SMEM_BUDGET 50000  // bytes of staged CSR tiles per merge CTA (stages = budget / tile bytes)
-#endif
 #ifndef MG_ITEMS
-#define MG_ITEMS 2048
+#define MG_ITEMS 0  // merge-path items per task; 0 = sized at plan time (about 16 tasks per resident warp)
+#endif
+#ifndef MW_U
+#define MW_U 8  // merge: B rows gathered per batch (row of <= 2 values per lane)
+#endif
+#ifndef MW_U4
+#define MW_U4 4  // merge: B rows per batch when a lane holds 3-4 values of a row (n > 64)
+#endif
+#ifndef MW_MINB
+#define MW_MINB 5  // merge: 256-thread CTAs per SM (40 warps, <= 48 registers; 6 x 40 registers spills)
+#endif
+#ifndef MW_MINB4
+#define MW_MINB4 5  // merge, 3-4 values of a row per lane
 #endif
 constexpr int kDefaultItems = MG_ITEMS;
 constexpr int kRowsplitU = RS_U;
-constexpr int kMergeU = MG_U;
-#ifndef RSP_U
-#define RSP_U 4
-#endif
-constexpr int kPairU = RSP_U;
 #ifndef RS_BSTAGE
 #define RS_BSTAGE 1  // row split: stage compact B row spans into shared memory with TMA (plan-time measured)
 #endif
@@ -108,10 +99,6 @@ constexpr int kPairU = RSP_U;
 #ifndef RS_BSTAGE_SMEM
 #define RS_BSTAGE_SMEM 110000  // shared-memory budget per CTA with B staging (2 CTAs per SM)
 #endif
-#ifndef RSP_MIN_SHARE
-#define RSP_MIN_SHARE 2.0  // row_pairing AUTO: pair when this fraction of nonzeros shares a B row (> 1: never)
-#endif
-
 spmm_status fail(spmm_csr_t h, spmm_status s, const std::string& msg) {
     if (h) h->err = msg;
     return s;
@@ -137,41 +124,6 @@ __global__ void k_max_row(const int* __restrict__ ro, long long m, int* __restri
         best = max(best, ro[i + 1] - ro[i]);
     best = __reduce_max_sync(FULL, best);
     if ((threadIdx.x & 31) == 0) atomicMax(out, best);
-}
-
-// Row-pair sharing measurement for spmm_plan_opts.row_pairing = AUTO: for every pair of rows (2i, 2i+1)
-// count the entries of row 2i+1 whose B row the pair kernel (tile.cuh) would share with row 2i, using the
-// kernel's own rule (entry j of Q pairs with entry j + delta of L, delta = #{L cols < Q's first col},
-// when the columns are equal; pairs with a row longer than 32 are not paired).  out[0] += shared,
-// out[1] += nonzeros of all pairs.
-__global__ void k_pair_share(const int* __restrict__ ro, const int* __restrict__ col, long long m,
-                             unsigned long long* __restrict__ out) {
-    unsigned long long shared = 0, total = 0;
-    const long long pairs = (m + 1) / 2;
-    for (long long pi = (long long)blockIdx.x * blockDim.x + threadIdx.x; pi < pairs;
-         pi += (long long)gridDim.x * blockDim.x) {
-        const long long l = 2 * pi;
-        const int sL = ro[l], eL = ro[l + 1];
-        const int eQ = (l + 1 < m) ? ro[l + 2] : eL;
-        total += (unsigned long long)(eQ - sL);
-        const int lenL = eL - sL, lenQ = eQ - eL;
-        if (lenL > 32 || lenQ > 32 || lenQ == 0) continue;
-        const int q0 = col[eL];
-        int delta = 0;
-        for (int i = 0; i < lenL; ++i) delta += (col[sL + i] < q0) ? 1 : 0;
-        for (int j = 0; j < lenQ; ++j) {
-            const int i = j + delta;
-            if (i < lenL && col[sL + i] == col[eL + j]) ++shared;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        shared += __shfl_down_sync(FULL, shared, o);
-        total += __shfl_down_sync(FULL, total, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&out[0], shared);
-        atomicAdd(&out[1], total);
-    }
 }
 
 // B-span compactness for the row-split kernel's B staging: warp per row tile of R rows; a tile is
@@ -254,9 +206,6 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
             c.G = G0;
             c.NV = (lanes + 31) / 32;
         }
-    } else if (MG_FOLD && n <= 16) {  // merge, small n: lane-folded workers of G lanes (32/G per warp)
-        c.G = pow2ceil(lanes);
-        c.NV = 1;
     } else {  // merge: one worker per warp, narrowest vector that covers n with 32 lanes
         const int want = n <= 32 ? 1 : (n <= 64 ? 2 : 4);
         if (want < vec) c.vec = want;
@@ -280,40 +229,42 @@ int num_sms() {
     return sms;
 }
 
-template <typename T, int SR, int MODE, int V, int G, int NV, int U, bool PAIR = false>
-cudaError_t launch_tile(TileParams P, cudaStream_t st) {
-    void (*kfn)(const TileParams);
-    if constexpr (PAIR) kfn = k_tile_pair<T, SR, V, G, NV, U>;
-    else kfn = k_tile<T, SR, MODE, V, G, NV, U>;
-    size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.n, P.stages, TE_CWARPS * (32 / G), MODE == MODE_MERGE,
-                                MODE == MODE_ROWSPLIT ? P.capb : 0);
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-#if TE_CARVE
-    // the carveout preference is sticky per kernel: size the occupancy query with the full shared
-    // memory array, not with the carveout an earlier (smaller) launch of this kernel asked for
-    e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-#endif
+// Kernel attributes are set and the occupancy is queried once per (kernel instance, device, shared
+// memory size) -- not on every execute (host overhead on the launch-bound small configs).
+struct LaunchCache {
+    int dev = -1;
+    size_t smem_set = 0;   // largest dynamic shared memory size set so far on `dev`
+    size_t smem_q = 0;     // shared memory size of the cached occupancy query
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, TE_THREADS, smem);
+};
+
+template <typename T, int SR, int MODE, int V, int G, int NV, int U>
+cudaError_t launch_tile(TileParams P, cudaStream_t st) {
+    void (*kfn)(const TileParams) = k_tile<T, SR, MODE, V, G, NV, U>;
+    static std::mutex mu;
+    static LaunchCache cache[8];
+    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.stages, P.capb);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (per_sm <= 0) return cudaErrorInvalidConfiguration;
-#if TE_CARVE
+    int per_sm = 0;
     {
-        // ask for the smallest shared-memory carveout that still fits the resident CTAs: the rest of the
-        // 228 KB unified array stays L1, which is where gathered B rows are reused (row split: every
-        // banded B row is read by 16 neighbouring rows)
-        const int want = std::min(per_sm, MODE == MODE_MERGE ? TE_MINB_MG : TE_MINB);  // pair kernels: 2 as row split
-        const size_t need = (size_t)want * (smem + 1024);
-        const int pct = (int)std::min<size_t>(100, (need * 100 + 228 * 1024 - 1) / (228 * 1024));
-        e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, TE_THREADS, smem);
-        if (e != cudaSuccess) return e;
-        if (per_sm <= 0) return cudaErrorInvalidConfiguration;
+        std::lock_guard<std::mutex> lock(mu);
+        LaunchCache& c = cache[dev & 7];
+        if (c.dev != dev) c = LaunchCache{dev, 0, 0, 0};
+        if (smem > c.smem_set) {
+            e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            c.smem_set = smem;
+        }
+        if (c.per_sm == 0 || c.smem_q != smem) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.per_sm, kfn, TE_THREADS, smem);
+            if (e != cudaSuccess) { c.per_sm = 0; return e; }
+            c.smem_q = smem;
+        }
+        per_sm = c.per_sm;
     }
-#endif
+    if (per_sm <= 0) return cudaErrorInvalidConfiguration;
     const long long grid = std::min<long long>(P.num_ranges, (long long)per_sm * num_sms());
     if (grid <= 0) return cudaSuccess;
     kfn<<<(unsigned)grid, TE_THREADS, smem, st>>>(P);
@@ -329,28 +280,17 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
     P.stages = RS_STAGES;
     // B staging needs 16-byte aligned B rows (TMA bulk copy source)
     P.capb = (h->capb > 0 && ((uintptr_t)P.B % 16) == 0 && (P.ldb_bytes % 16) == 0) ? h->capb : 0;
-    mark(h, 0, st);
     cudaError_t e;
+    mark(h, 0, st);
+    int ev = 1;
     if (h->rs_dyn) {
-        // irregular row lengths: row tiles from a queue in the workspace, zeroed here
+        // irregular row lengths: row tiles from a queue in the workspace, zeroed here;
+        // counted as launch 0 of the execute (spmm_plan_info.launches_per_execute / compute_launch)
         e = cudaMemsetAsync(P.tile_ctr, 0, sizeof(int), st);
         if (e != cudaSuccess) return e;
+        mark(h, ev++, st);
     } else {
         P.tile_ctr = nullptr;
-    }
-    if (h->pairing) {
-        e = cudaErrorNotSupported;
-#define RSP_CASE(V, G_, NV_) \
-    case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kPairU, true>(P, st); break;
-        switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
-            RSP_CASE(4, 2, 1) RSP_CASE(4, 4, 1) RSP_CASE(4, 8, 1) RSP_CASE(4, 8, 2) RSP_CASE(4, 16, 2)
-            default: break;
-        }
-#undef RSP_CASE
-        if (e != cudaErrorNotSupported) {  // no pair instance for this vector shape: plain row split
-            mark(h, 1, st);
-            return e;
-        }
     }
 #define RS_CASE(V, G_, NV_) \
     case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kRowsplitU>(P, st); break;
@@ -364,8 +304,62 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
         default: return cudaErrorNotSupported;
     }
 #undef RS_CASE
-    mark(h, 1, st);
+    mark(h, ev, st);
     return e;
+}
+
+// k_merge_w launch; with M == nullptr only the resident CTAs per SM are returned in *per_sm_out
+// (plan sizes the merge-path tasks from it: one task per resident worker by default)
+template <typename T, int SR, int V, int NV, int U, int MB>
+cudaError_t launch_merge_w(const MergeParams* M, cudaStream_t st, int* per_sm_out = nullptr) {
+    void (*kfn)(const MergeParams) = k_merge_w<T, SR, V, NV, U, MB>;
+    static std::mutex mu;
+    static int per_sm_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int per_sm;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        int& c = per_sm_cache[dev & 7];
+        if (c == 0) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kfn, MW_THREADS, 0);
+            if (e != cudaSuccess) { c = 0; return e; }
+        }
+        per_sm = c;
+    }
+    if (per_sm <= 0) return cudaErrorInvalidConfiguration;
+    if (per_sm_out) *per_sm_out = per_sm;
+    if (!M) return cudaSuccess;
+    const long long grid = std::min<long long>((M->num_tasks + MW_THREADS / 32 - 1) / (MW_THREADS / 32),
+                                               (long long)per_sm * num_sms());
+    if (grid <= 0) return cudaSuccess;
+    kfn<<<(unsigned)grid, MW_THREADS, 0, st>>>(*M);
+    return cudaGetLastError();
+}
+
+// dispatch over the k_merge_w instances by vector shape (pick_vec with G = 32)
+template <typename T, int SR>
+cudaError_t dispatch_merge_w(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out) {
+#define MW_CASE(V, NV_, U_, MB_) \
+    case (V)*10 + (NV_): return launch_merge_w<T, SR, V, NV_, U_, MB_>(M, st, per_sm_out);
+    switch (cfg.vec * 10 + cfg.NV) {
+        MW_CASE(4, 1, MW_U4, MW_MINB4) MW_CASE(2, 1, MW_U, MW_MINB) MW_CASE(2, 2, MW_U4, MW_MINB4)
+        MW_CASE(1, 1, MW_U, MW_MINB) MW_CASE(1, 2, MW_U, MW_MINB) MW_CASE(1, 3, MW_U4, MW_MINB4)
+        MW_CASE(1, 4, MW_U4, MW_MINB4)
+        default: return cudaErrorNotSupported;
+    }
+#undef MW_CASE
+}
+
+int merge_w_per_sm(spmm_dtype dt, spmm_semiring sr, VecCfg cfg) {
+    int per_sm = 0;
+    cudaError_t e;
+    if (dt == SPMM_F32) e = sr == SPMM_PLUS_TIMES ? dispatch_merge_w<float, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                                  : dispatch_merge_w<float, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    else e = sr == SPMM_PLUS_TIMES ? dispatch_merge_w<int, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                   : dispatch_merge_w<int, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    return e == cudaSuccess ? per_sm : 0;
 }
 
 template <typename T, int SR>
@@ -380,39 +374,26 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     off += align256(sizeof(int) * NC);
     T* carry_val = reinterpret_cast<T*>(ws + off);
     off += align256(sizeof(T) * (size_t)NC * h->n);
-    int* tile_ctr = MG_DYN ? reinterpret_cast<int*>(ws + off) : nullptr;
     const int items = h->items;
     // phase 1: PartitionSpmm (Alg. 1 line 2)
     const long long pgrid = (NC + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     mark(h, 0, st);
     k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, (int)h->m, (int)h->nnz, items, h->opts.partition, (int)NC,
-                                                     states, tile_ctr);
+                                                     states);
     mark(h, 1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // phase 2: per-CTA compute + carry-out (Alg. 1 lines 3-23)
-    P.num_ranges = (int)NC;
-    P.states = states;
-    P.items = items;
-    P.carry_row = carry_row;
-    P.carry_flag = carry_flag;
-    P.carry_val = carry_val;
-    P.tile_ctr = tile_ctr;
-    P.capr = items + 8;
-    P.capz = items + 8;
-    P.stages = std::max(2, std::min(TE_MAX_STAGES, (int)(MG_SMEM_BUDGET / te_buf_bytes(P.capr, P.capz, (int)sizeof(T)))));
-#define MG_CASE(V, G_, NV_) \
-    case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_MERGE, V, G_, NV_, kMergeU>(P, st); break;
-    switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
-        MG_CASE(4, 32, 1) MG_CASE(2, 32, 1) MG_CASE(2, 32, 2) MG_CASE(1, 32, 1) MG_CASE(1, 32, 2) MG_CASE(1, 32, 3)
-        MG_CASE(1, 32, 4)
-#if MG_FOLD
-        MG_CASE(4, 1, 1) MG_CASE(4, 2, 1) MG_CASE(4, 4, 1) MG_CASE(2, 1, 1) MG_CASE(2, 2, 1) MG_CASE(2, 4, 1)
-        MG_CASE(2, 8, 1) MG_CASE(1, 1, 1) MG_CASE(1, 2, 1) MG_CASE(1, 4, 1) MG_CASE(1, 8, 1) MG_CASE(1, 16, 1)
-#endif
-        default: return cudaErrorNotSupported;
-    }
-#undef MG_CASE
+    // phase 2: per-task compute + carry-out (Alg. 1 lines 3-23)
+    MergeParams M{};
+    M.m = P.m; M.n = P.n; M.nnz = P.nnz;
+    M.ro = P.ro; M.col = P.col; M.val = P.val;
+    M.B = P.B; M.ldb_bytes = P.ldb_bytes; M.C = P.C; M.ldc = P.ldc;
+    M.states = states;
+    M.num_tasks = (int)NC;
+    M.carry_row = carry_row;
+    M.carry_flag = carry_flag;
+    M.carry_val = carry_val;
+    e = dispatch_merge_w<T, SR>(cfg, &M, st, nullptr);
     mark(h, 2, st);
     if (e != cudaSuccess) return e;
     // phase 3: FixCarryOut (Alg. 1 line 24)
@@ -567,14 +548,27 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     if (opts) o = *opts;
     for (int i = 0; i < 4; ++i)
         if (o.reserved[i] != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
-    if (o.row_pairing != SPMM_PAIRING_AUTO && o.row_pairing != SPMM_PAIRING_OFF && o.row_pairing != SPMM_PAIRING_ON)
-        return fail(h, SPMM_ERR_INVALID_ARG, "bad row_pairing");
+    if (o.reserved0 != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
     if (o.policy != SPMM_POLICY_AUTO && o.policy != SPMM_POLICY_PAPER) return fail(h, SPMM_ERR_INVALID_ARG, "bad policy");
     if (o.partition != SPMM_PARTITION_MERGE_PATH && o.partition != SPMM_PARTITION_NONZERO_SPLIT)
         return fail(h, SPMM_ERR_INVALID_ARG, "bad partition");
     int items = o.items_per_cta ? o.items_per_cta : kDefaultItems;
-    if (items < 256 || items > 4096 || items % 256 != 0)
-        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 256 in [256, 4096]");
+    if (items == 0 && !(algo == SPMM_ALGO_ROWSPLIT)) {
+        // merge-path items per task (the partition granularity, Alg. 1 line 2): one task per resident
+        // merge worker (warp) of the kernel instance this n uses with aligned B / C, so every worker
+        // streams one contiguous, equal slice of the path and there is one carry-out per worker
+        const VecCfg mc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, false);
+        int per_sm = merge_w_per_sm(h->dtype, sr, mc);
+        if (per_sm <= 0) per_sm = MW_MINB;
+        const long long workers = (long long)num_sms() * per_sm * (MW_THREADS / 32);
+        const long long path = o.partition == SPMM_PARTITION_NONZERO_SPLIT ? h->nnz : h->m + h->nnz;
+        long long it = (path + workers - 1) / workers;
+        it = std::max<long long>(256, (it + 31) / 32 * 32);
+        items = (int)std::min<long long>(it, 1LL << 30);
+    }
+    if (items == 0) items = 256;  // forced row split: unused
+    if (items < 32 || items > (1 << 30) || items % 32 != 0)
+        return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 32 in [32, 2^30]");
     o.items_per_cta = items;
     h->threshold = threshold > 0 ? threshold : 9.35;
     h->n = n;
@@ -582,8 +576,6 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     h->opts = o;
     h->items = items;
     h->max_row = -1;
-    h->pairing = false;
-    h->pair_shared = -1.0;
     h->capb = 0;
     h->bspan_compact = -1.0;
     h->rs_dyn = false;
@@ -624,7 +616,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         if (NC > 0) {
             const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
             h->ws_bytes = align256(sizeof(int) * 2 * (NC + 1)) + 2 * align256(sizeof(int) * NC) +
-                          align256(elem * (size_t)NC * n) + (MG_DYN ? 256 : 0);
+                          align256(elem * (size_t)NC * n);
         }
     } else {
         // row tiles of R rows sized so a typical tile's nonzeros fit the staged shared-memory slice
@@ -690,25 +682,6 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         h->rs_dyn = o.policy == SPMM_POLICY_AUTO && h->max_row >= 0 &&
                     (double)h->max_row > RS_DYN_SKEW * std::max(1.0, d);
         if (h->rs_dyn) h->ws_bytes = 256;
-        if (o.row_pairing == SPMM_PAIRING_ON) {
-            h->pairing = true;
-        } else if (o.row_pairing == SPMM_PAIRING_AUTO && o.policy == SPMM_POLICY_AUTO && h->nnz > 0 && h->m > 1) {
-            cudaStream_t st = static_cast<cudaStream_t>(stream);
-            unsigned long long cnt[2] = {0, 0};
-            unsigned long long* dc = reinterpret_cast<unsigned long long*>(h->d_scratch + 4);
-            cudaError_t e = cudaMemsetAsync(dc, 0, 2 * sizeof(unsigned long long), st);
-            if (e == cudaSuccess) {
-                const long long pairs = (h->m + 1) / 2;
-                const int grid = (int)std::min<long long>((pairs + THREADS - 1) / THREADS, 8LL * kNumSMs);
-                k_pair_share<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, dc);
-                e = cudaGetLastError();
-            }
-            if (e == cudaSuccess) e = cudaMemcpyAsync(cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return cuda_fail(h, e, "plan: row-pair sharing");
-            h->pair_shared = cnt[1] ? (double)cnt[0] / (double)cnt[1] : 0.0;
-            h->pairing = h->pair_shared >= RSP_MIN_SHARE;
-        }
     }
     h->planned = true;
     if (workspace_bytes) *workspace_bytes = h->ws_bytes;
@@ -733,8 +706,8 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
     out->threshold = h->threshold;
     out->num_ctas = (int32_t)h->num_ctas;
     out->items_per_cta = h->chosen == SPMM_ALGO_MERGE ? h->items : 0;
-    out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : 1);
-    out->row_pairing = (h->chosen == SPMM_ALGO_ROWSPLIT && h->pairing) ? 1 : 0;
+    out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : (h->rs_dyn ? 2 : 1));
+    out->compute_launch = (h->chosen == SPMM_ALGO_MERGE || h->rs_dyn) ? 1 : 0;
     out->b_staging = (h->chosen == SPMM_ALGO_ROWSPLIT && h->capb > 0) ? 1 : 0;
     out->rows_per_tile = h->chosen == SPMM_ALGO_ROWSPLIT ? h->rows_per_tile : 0;
     out->bspan_compact = h->bspan_compact;

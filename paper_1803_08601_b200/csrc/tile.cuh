@@ -1,5 +1,5 @@
-// tile.cuh -- the sm_100a compute kernel shared by both of the paper's algorithms: a persistent,
-// warp-specialised "tile engine".
+// tile.cuh -- Algorithm I, row-splitting SpMM (§4.1), as a persistent,
+// warp-specialised "tile engine" for sm_100a.  (Algorithm II, merge-based, is merge_w.cuh.)
 //
 //   warp 8 (producer, one elected lane issues): walks this CTA's tiles, computes each tile's bounds
 //     and stages the tile's slice of A -- row offsets, column indices, values -- into shared memory
@@ -12,17 +12,12 @@
 //     float2 loads of row-major B), U gathers in flight before the first FMA (ILP,
 //     PAPER.md:55-57), accumulate with packed FFMA2, and write finished rows of C with streaming stores.
 //
-// MODE_ROWSPLIT (Algorithm I, §4.1): a tile is a fixed block of rows; each row is owned by one group
-//   of G lanes (G = ceil(n/VEC) rounded to a power of two, so a warp runs 32/G rows); no carries.
-// MODE_MERGE (Algorithm II, §4.2): a tile is one CTA range of the merge-path partition (k_partition,
-//   Alg. 1 line 2); each warp takes an equal share of the tile's items (rows + nonzeros) by a second
-//   merge-path search in shared memory and streams them; carry-outs are resolved in the CTA and the
-//   CTA's open row goes to the global carry array for k_fixup (Alg. 1 lines 22-24).
+// A tile is a fixed block of rows; each row is owned by one group of G lanes (G = ceil(n/VEC) rounded
+// to a power of two, so a warp runs 32/G rows); no carries.
 #pragma once
 #include <type_traits>
 
 #include "common.cuh"
-#include "merge.cuh"
 #include "ptx.cuh"
 
 namespace spmm {
@@ -32,15 +27,11 @@ namespace spmm {
 #endif
 constexpr int TE_CWARPS = TE_CWARPS_DEF;        // consumer warps
 constexpr int TE_THREADS = 32 * (TE_CWARPS + 1);  // + 1 producer warp
-constexpr int TE_CONSUMERS = 32 * TE_CWARPS;
 #ifndef TE_MINB
 #define TE_MINB 2  // row split: CTAs per SM the register allocation targets (__launch_bounds__)
 #endif
-#ifndef TE_MINB_MG
-#define TE_MINB_MG 4  // merge: CTAs per SM (random gathers want many warps: TLP over ILP)
-#endif
 constexpr int TE_MAX_STAGES = 8;                // shared-memory pipeline depth limit (tiles in flight)
-enum : int { MODE_ROWSPLIT = 0, MODE_MERGE = 1 };
+enum : int { MODE_ROWSPLIT = 0 };
 
 struct TileParams {
     int m, n, nnz;
@@ -51,26 +42,21 @@ struct TileParams {
     unsigned ldb_bytes;  // ldb * sizeof(T) (< 2^32)
     void* C;
     long long ldc;
-    int num_ranges;     // rowsplit: row tiles; merge: partition CTAs
-    int rows_per_tile;  // rowsplit
-    const int* states;  // merge: (row, nz) per range boundary
-    int items;          // merge: items per sub-tile (shared-memory capacity)
-    int* carry_row;
-    int* carry_flag;
-    void* carry_val;
+    int num_ranges;     // row tiles
+    int rows_per_tile;
     int capr, capz;     // elements per buffer: row offsets / (col, val)
     unsigned pf_bytes;  // bytes of each B row to prefetch into L2 ahead of the consumers (0 = off)
     int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
     int capb;           // rowsplit: bytes per stage for the tile's B row span (0 = B is gathered from global)
-    int* tile_ctr;      // merge, MG_DYN: global tile queue (zeroed by k_partition); null = static round robin
+    int* tile_ctr;      // tile queue (irregular rows; zeroed before the launch); null = static round robin
 };
 
 // tile descriptor written by the producer next to the staged data
 struct TileInfo {
-    int rs, zs, re, ze;  // merge-path state at tile start / end (rowsplit: zs = ro[rs], ze = ro[re])
+    int rs, zs, re, ze;  // rows [rs, re) of the tile, nonzeros [zs = ro[rs], ze = ro[re])
     int ebase, zbase;    // global index of E[0] and of COL[0]/VAL[0]
-    int range;           // partition range (merge) / row tile (rowsplit)
-    int flags;           // 1 first sub-tile of range, 2 last sub-tile, 4 staged, 8 done, 16 B span staged
+    int range;           // row tile
+    int flags;           // 1 first sub-tile, 2 last sub-tile, 4 staged, 8 done, 16 B span staged
     int blo;             // flags & 16: B row held at the start of the staged B span
 };
 
@@ -79,14 +65,9 @@ __host__ __device__ inline size_t te_buf_bytes(int capr, int capz, int elem, int
     return (size_t)capr * 4 + (size_t)capz * 4 + (size_t)capz * elem + 64 + (size_t)capb;
 }
 constexpr int TE_BAR_BYTES = 24 * TE_MAX_STAGES;  // full / empty / csr-landed mbarriers
-// nw = merge workers per CTA (consumer warps x row groups per warp); row split needs no carry slots,
-// and every byte of shared memory it does not claim stays L1 (unified carveout) for B-row reuse
-__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int n, int stages, int nw, bool merge,
-                                                int capb = 0) {
-    const size_t base = stages * te_buf_bytes(capr, capz, elem, capb) + TE_BAR_BYTES;
-    if (!merge) return base;
-    return base + (size_t)(nw + 1) * n * elem + (size_t)(nw + 1) * 8 + 64 +
-           (size_t)stages * nw * n * elem + (size_t)stages * nw * 8 + stages * 4 + 64;
+// every byte of shared memory the tile engine does not claim stays L1 (unified carveout) for B-row reuse
+__host__ __device__ inline size_t te_smem_bytes(int capr, int capz, int elem, int stages, int capb = 0) {
+    return stages * te_buf_bytes(capr, capz, elem, capb) + TE_BAR_BYTES;
 }
 
 // stage global src[begin, end) (4-byte elements, arr_len elements in the array) at dst; returns the
@@ -187,12 +168,12 @@ template <typename T, int SR, int VEC, int NV> struct Acc {
     }
 };
 
-template <typename T, int SR, int MODE, int VEC, int G, int NV, int U, bool PAIR>
+template <typename T, int SR, int MODE, int VEC, int G, int NV, int U>
 __device__ __forceinline__ void tile_body(const TileParams& P) {
     using R = Ring<T, SR>;
     extern __shared__ __align__(128) unsigned char smem[];
     const int capr = P.capr, capz = P.capz, n = P.n, m = P.m;
-    const size_t bufb = te_buf_bytes(capr, capz, (int)sizeof(T), MODE == MODE_ROWSPLIT ? P.capb : 0);
+    const size_t bufb = te_buf_bytes(capr, capz, (int)sizeof(T), P.capb);
     auto E_of = [&](int b) { return reinterpret_cast<int*>(smem + b * bufb); };
     auto COL_of = [&](int b) { return reinterpret_cast<int*>(smem + b * bufb + (size_t)capr * 4); };
     auto VAL_of = [&](int b) { return reinterpret_cast<T*>(smem + b * bufb + (size_t)capr * 4 + (size_t)capz * 4); };
@@ -204,15 +185,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * bufb);
     uint64_t* empty = full + TE_MAX_STAGES;
     uint64_t* landed = empty + TE_MAX_STAGES;  // rowsplit + B staging: the tile's CSR slice has landed
-    T* Cw = reinterpret_cast<T*>(smem + NS * bufb + TE_BAR_BYTES);                 // [W+1][n] worker carries
-    constexpr int NWK = TE_CWARPS * (32 / G);  // merge workers per CTA
-    int* Crow = reinterpret_cast<int*>(Cw + (size_t)(NWK + 1) * n);  // [NWK+1]
-    int* Cflag = Crow + (NWK + 1);                                   // [NWK+1]
-    // per-stage worker carry slots for the barrier-free resolution of single-tile ranges
-    T* CwS = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(Cflag + (NWK + 1)) + 64);  // [S][NWK][n]
-    int* CrowS = reinterpret_cast<int*>(CwS + (size_t)NS * NWK * n);                   // [S][NWK]
-    int* CflagS = CrowS + NS * NWK;                                                     // [S][NWK]
-    int* Ccnt = CflagS + NS * NWK;                                                      // [S]
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -293,7 +265,9 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 lo = __reduce_min_sync(FULL, lo);
                 hi = __reduce_max_sync(FULL, hi);
                 const long long span = (long long)hi - lo + 1;
-                const long long bytes = span * (long long)P.ldb_bytes;
+                // rows lo..hi at pitch ldb, the last one only up to column n (never past B's last
+                // element; B staging is planned only when n * sizeof(T) is a multiple of 16)
+                const long long bytes = (span - 1) * (long long)P.ldb_bytes + (long long)n * (long long)sizeof(T);
                 if (span <= 2LL * cnt && bytes <= P.capb) {
                     if (lane == 0) {
                         fence_proxy_async_smem();
@@ -310,7 +284,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             __syncwarp();
             if (lane == 0) mbar_arrive_expect_tx(&full[pb], btx);
         };
-        const bool bstage = MODE == MODE_ROWSPLIT && P.capb > 0;
+        const bool bstage = P.capb > 0;
         const bool val_tma = te_phase(P.col) == te_phase(P.val);
         int pend = -1;  // B staging: tile index whose CSR slice is in flight
         // tiles: static round robin, or (merge; row split with irregular rows) taken from a global queue
@@ -324,29 +298,14 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             return cur < 0 ? (int)blockIdx.x : cur + (int)gridDim.x;
         };
         for (int c = next_tile(-1); c < P.num_ranges; c = next_tile(c)) {
-            long long rs, zs, re, ze;
-            if (MODE == MODE_ROWSPLIT) {
-                rs = (long long)c * P.rows_per_tile;
-                re = min((long long)m, rs + P.rows_per_tile);
-                zs = ld_stream(P.ro + rs);
-                ze = ld_stream(P.ro + re);
-            } else {
-                rs = P.states[2 * c];
-                zs = P.states[2 * c + 1];
-                re = P.states[2 * c + 2];
-                ze = P.states[2 * c + 3];
-            }
+            const long long rs = (long long)c * P.rows_per_tile;
+            const long long re = min((long long)m, rs + P.rows_per_tile);
+            const long long zs = ld_stream(P.ro + rs);
+            const long long ze = ld_stream(P.ro + re);
             long long cr = rs, cz = zs;  // current sub-tile start
             bool first = true;
             while (true) {
-                long long nr = re, nz = ze;
-                if (MODE == MODE_MERGE && (re - cr) + (ze - cz) > P.items) {
-                    // oversize range (1-D nonzero split with many rows): cut at diagonal +items
-                    const long long D = cr + cz + P.items;
-                    const long long lo = max(cr, D - ze), hi = min(D - cz, re);
-                    nr = warp_search_first(lo, hi, MergePred{P.ro, D});
-                    nz = D - nr;
-                }
+                const long long nr = re, nz = ze;
                 const bool last = (nr == re && nz == ze);
                 int b;
                 acquire(b);
@@ -358,16 +317,9 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                     inf.blo = 0;
                     inf.rs = (int)cr; inf.zs = (int)cz; inf.re = (int)nr; inf.ze = (int)nz;
                     inf.range = c;
-                    bool staged;
                     fence_proxy_async_smem();
-                    if (MODE == MODE_ROWSPLIT) {
-                        staged = (nz - cz) + 8 <= capz;
-                        inf.ebase = te_stage(E_of(b), P.ro, cr, nr + 1, (long long)m + 1, csr_bar, pol, &tx);
-                    } else {
-                        staged = true;
-                        const long long e1 = min(nr + 1, (long long)m);  // row ends of rows cr..min(nr, m-1)
-                        inf.ebase = te_stage(E_of(b), P.ro, cr + 1, e1 + 1, (long long)m + 1, &full[b], pol, &tx);
-                    }
+                    const bool staged = (nz - cz) + 8 <= capz;
+                    inf.ebase = te_stage(E_of(b), P.ro, cr, nr + 1, (long long)m + 1, csr_bar, pol, &tx);
                     if (staged) {
                         inf.zbase = te_stage(COL_of(b), P.col, cz, nz, P.nnz, csr_bar, pol, &tx);
                         // values share the column indices' index base when both arrays have the same
@@ -398,7 +350,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 if (bstage) {
                     if (pend >= 0) finish_tile(pend % NS, pend);  // overlaps this tile's CSR load
                     pend = i;
-                } else if (MODE == MODE_ROWSPLIT && P.pf_bytes && i >= 1) {
+                } else if (P.pf_bytes && i >= 1) {
                     prefetch_tile_b((i - 1) % NS, i - 1);
                 }
                 ++i;
@@ -428,7 +380,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
 #ifndef RS_NA
 #define RS_NA 1  // row split: one accumulator set per row (measured 1-7% faster than 2 interleaved)
 #endif
-    constexpr int NA = (MODE == MODE_MERGE) ? ((VEC * NV <= 2) ? MG_NA : 2) : RS_NA;
+    constexpr int NA = RS_NA;
     const int slot = lane / G;
     const int gl = lane - slot * G;
     bool colok[NV];
@@ -475,12 +427,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
         }
     };
 
-    if (MODE == MODE_MERGE && threadIdx.x == 0) {
-        Crow[NWK] = -1;
-        Cflag[NWK] = 0;
-        for (int s = 0; s < NS; ++s) Ccnt[s] = 0;
-    }
-    if (MODE == MODE_MERGE) named_bar_sync(1, TE_CONSUMERS);
 
     for (int i = 0;; ++i) {
         const int b = i % NS;
@@ -582,149 +528,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                     }
                 }
             };
-            bool tile_done = false;
-            if constexpr (PAIR) {
-                auto pair_body = [&]() {
-                    // Row pairs (B200 extension of §4.1), only for tiles whose B span is
-                    // staged in shared memory: a group owns rows (2i, 2i+1) = (L, Q).  Q's entry j is
-                    // matched with L's entry j + delta (delta = #{L cols < Q's first col}) when the two
-                    // columns are equal; the B row read for L's entry then also feeds Q, so a banded pair
-                    // reads 17 B rows into registers instead of 32.  Q's unmatched entries are read
-                    // afterwards.  Every stored entry is used exactly once whatever the column order, so
-                    // the result is C = AB for any CSR (sorted columns only make the matching effective).
-                    constexpr bool kS = true;
-                    const int pairs = (rows + 1) >> 1;
-                    const int prounds = (pairs + NG - 1) / NG;
-                    const uint32_t colz = smem_u32(COL) - 4u * (uint32_t)inf.zbase;  // + 4p: column of nonzero p
-                    const uint32_t valz = smem_u32(VAL) - 4u * (uint32_t)inf.zbase;
-                    const unsigned gbits = (G == 32) ? 0xffffffffu : ((1u << G) - 1u);
-                    for (int t = 0; t < prounds; ++t) {
-                        const int lr = 2 * (t * NG + gid);
-                        const bool actL = lr < rows;
-                        const bool actQ = lr + 1 < rows;
-                        const int sL = actL ? E[inf.rs + lr - inf.ebase] : 0;
-                        const int eL = actL ? E[inf.rs + lr + 1 - inf.ebase] : 0;
-                        const int eQ = actQ ? E[inf.rs + lr + 2 - inf.ebase] : eL;
-                        const int lenL = eL - sL, lenQ = eQ - eL;
-                        if (!__all_sync(FULL, lenL <= 32 && lenQ <= 32)) {
-                            // a long row in the warp: the two rows one after the other (plain row split)
-#pragma unroll 1
-                            for (int h = 0; h < 2; ++h) {
-                                Acc<T, SR, VEC, NV> accs[NA];
-#pragma unroll
-                                for (int k = 0; k < NA; ++k) accs[k].reset();
-                                row_pass(kS, h ? eL : sL, h ? lenQ : lenL, accs);
-#pragma unroll
-                                for (int k = 1; k < NA; ++k) accs[0].fold(accs[k]);
-                                store_row(inf.rs + lr + h, accs[0], h ? actQ : actL);
-                            }
-                            continue;
-                        }
-                        const int maxL = __reduce_max_sync(FULL, lenL);
-                        const int maxQ = __reduce_max_sync(FULL, lenQ);
-                        // delta and the match mask, the group's lanes in parallel
-                        const int q0 = (lenQ > 0) ? (int)lds_u32(colz + 4u * (uint32_t)eL) : 0x7fffffff;
-                        int delta = 0;
-                        for (int k0 = 0; k0 < maxL; k0 += G) {
-                            const int i = k0 + gl;
-                            const bool in = i < lenL;
-                            const bool lt = in && (int)lds_pred(colz + 4u * (uint32_t)(sL + i), in) < q0;
-                            delta += __popc((__ballot_sync(FULL, lt) >> (slot * G)) & gbits);
-                        }
-                        uint32_t mask = 0;  // bit j: Q's entry j is paired with L's entry j + delta
-                        for (int k0 = 0; k0 < maxQ; k0 += G) {
-                            const int j = k0 + gl;
-                            const bool in = j < lenQ && j + delta < lenL;
-                            const unsigned a = lds_pred(colz + 4u * (uint32_t)(eL + j), in);
-                            const unsigned c = lds_pred(colz + 4u * (uint32_t)(sL + j + delta), in);
-                            const unsigned bits = (__ballot_sync(FULL, in && a == c) >> (slot * G)) & gbits;
-                            mask |= bits << k0;
-                        }
-                        Acc<T, SR, VEC, NV> accL, accQ;
-                        accL.reset();
-                        accQ.reset();
-                        // L's batches in an order rotated by the group's slot (bank spread)
-                        const int nb = (maxL + U - 1) / U;
-                        int bb = slot % nb;
-                        for (int bi = 0; bi < nb; ++bi) {
-                            const int p0 = bb * U;
-                            bb = (bb + 1 == nb) ? 0 : bb + 1;
-                            const int rem = lenL - p0;
-                            unsigned bv[U][NV][VEC];
-                            unsigned cu[U], av[U], aq[U];
-                            const uint32_t ca = colz + 4u * (uint32_t)(sL + p0);
-                            const uint32_t va = valz + 4u * (uint32_t)(sL + p0);
-                            // mask bits of Q entries p0 - delta .. p0 - delta + U - 1 (p0 - delta < 32)
-                            const int j0 = p0 - delta;
-                            const uint32_t mw = (j0 >= 0) ? (mask >> j0) : (j0 > -32 ? (mask << -j0) : 0u);
-                            if (U % 4 == 0 && __all_sync(FULL, rem >= U && (ca & 15u) == 0)) {
-                                // full batch for every group: unpredicated loads; Q's values are read
-                                // unconditionally (eL + j0 + u >= sL stays inside the stage buffer) and
-                                // used only where the mask says the entry is paired
-#pragma unroll
-                                for (int u = 0; u < U; u += 4) {
-                                    const uint4 c4 = lds_u128(ca + 4u * u);
-                                    const uint4 a4 = lds_u128(va + 4u * u);
-                                    cu[u] = c4.x; cu[u + 1] = c4.y; cu[u + 2] = c4.z; cu[u + 3] = c4.w;
-                                    av[u] = a4.x; av[u + 1] = a4.y; av[u + 2] = a4.z; av[u + 3] = a4.w;
-                                }
-#pragma unroll
-                                for (int u = 0; u < U; ++u) aq[u] = lds_u32(valz + 4u * (uint32_t)(eL + j0 + u));
-#pragma unroll
-                                for (int u = 0; u < U; ++u) GF(kS, bv[u], (int)cu[u]);
-#pragma unroll
-                                for (int u = 0; u < U; ++u) {
-                                    accL.mac(from_bits<T>(av[u]), bv[u]);
-                                    if ((mw >> u) & 1u) accQ.mac(from_bits<T>(aq[u]), bv[u]);
-                                }
-                                continue;
-                            }
-#pragma unroll
-                            for (int u = 0; u < U; ++u) {
-                                cu[u] = lds_pred(ca + 4u * u, u < rem);
-                                av[u] = lds_pred(va + 4u * u, u < rem);
-                            }
-#pragma unroll
-                            for (int u = 0; u < U; ++u)
-                                aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j0 + u), (mw >> u) & 1u);
-#pragma unroll
-                            for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], u < rem);
-#pragma unroll
-                            for (int u = 0; u < U; ++u) {
-                                if (u < rem) accL.mac(from_bits<T>(av[u]), bv[u]);
-                                if ((mw >> u) & 1u) accQ.mac(from_bits<T>(aq[u]), bv[u]);
-                            }
-                        }
-                        // Q's entries without a partner
-                        uint32_t todo = (lenQ >= 32 ? 0xffffffffu : ((1u << lenQ) - 1u)) & ~mask;
-                        const int maxc = __reduce_max_sync(FULL, __popc(todo));
-                        for (int c0 = 0; c0 < maxc; c0 += U) {
-                            unsigned bv[U][NV][VEC];
-                            unsigned aq[U];
-                            bool ok[U];
-#pragma unroll
-                            for (int u = 0; u < U; ++u) {
-                                ok[u] = todo != 0u;
-                                const int j = ok[u] ? __ffs((int)todo) - 1 : 0;
-                                todo &= todo - 1u;
-                                const unsigned cq = lds_pred(colz + 4u * (uint32_t)(eL + j), ok[u]);
-                                aq[u] = lds_pred(valz + 4u * (uint32_t)(eL + j), ok[u]);
-                                if (c0 + u < maxc) GP(kS, bv[u], (int)cq, ok[u]);
-                            }
-#pragma unroll
-                            for (int u = 0; u < U; ++u)
-                                if (ok[u]) accQ.mac(from_bits<T>(aq[u]), bv[u]);
-                        }
-                        store_row(inf.rs + lr, accL, actL);
-                        store_row(inf.rs + lr + 1, accQ, actQ);
-                    }
-                };
-                if (staged && bsm) {  // pairs only from a staged B span (short latencies); else plain rows
-                    pair_body();
-                    tile_done = true;
-                }
-            }
-            if (!tile_done) {
+            {
                 const int rounds = (rows + NG - 1) / NG;
                 for (int t = 0; t < rounds; ++t) {
                     const int lr = t * NG + gid;
@@ -743,292 +547,13 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[b]);
-        } else {
-            // ---------------- Algorithm II: merge-path items; a worker = a warp (G = 32) or, for
-            // small n, a group of G lanes (32/G independent workers per warp, lane folding) ----------
-            const int rs = inf.rs, zs = inf.zs, re = inf.re, ze = inf.ze;
-            const int L = (re - rs) + (ze - zs);
-            const int wid = warp * S + slot;  // worker id, ascending along the merge path
-            const int per = (L + NWK - 1) / NWK;
-            const int* Eb = E + 1 - inf.ebase;  // Eb[x] = ro[x+1] (row end of row x)
-            auto search = [&](int d) -> int {
-                const int D = rs + zs + d;
-                int lo = max(rs, D - ze), hi = min(D - zs, re);
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (Eb[mid] <= D - mid - 1) lo = mid + 1; else hi = mid;
-                }
-                return lo;
-            };
-            const int d0 = min(wid * per, L), d1 = min((wid + 1) * per, L);
-            const int ia = search(d0), ja = rs + zs + d0 - ia;
-            const int ib = search(d1), jb = rs + zs + d1 - ib;
-
-            Acc<T, SR, VEC, NV> accs[NA];  // NA interleaved partial sums: short FMA dependency chains
-#pragma unroll
-            for (int k = 1; k < NA; ++k) accs[k].reset();
-            Acc<T, SR, VEC, NV>& acc = accs[0];
-            bool dirty = false;
-            if (wid == 0 && !(inf.flags & 1) && Cflag[NWK]) {  // carry-in from the previous sub-tile
-#pragma unroll
-                for (int v = 0; v < NV; ++v)
-#pragma unroll
-                    for (int x = 0; x < VEC; ++x) {
-                        const int cc = cofs[v] + x;
-                        acc.v[v][x] = (cc < n) ? Cw[NWK * n + cc] : R::id();
-                    }
-                dirty = true;
-            } else {
-                acc.reset();
-            }
-            int r = ia, q = ja;
-            int e = (r < m) ? Eb[r] : 0x7fffffff;
-            auto collapse = [&]() {
-#pragma unroll
-                for (int k = 1; k < NA; ++k) {
-                    accs[0].fold(accs[k]);
-                    accs[k].reset();
-                }
-            };
-            auto flush = [&]() {
-                collapse();
-                store_row(r, acc, true);
-                acc.reset();
-                dirty = false;
-                ++r;
-                e = (r < m) ? Eb[r] : 0x7fffffff;
-            };
-          if constexpr (G == 32) {
-            while (q < jb) {
-                const int cnt = min(U, jb - q);
-                unsigned bv[U][NV][VEC];
-                T av[U];
-                const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(q - inf.zbase);
-                const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(q - inf.zbase);
-                unsigned cu[U], au[U];
-                if (cnt == U && q + U <= e) {  // full batch inside the current row: no row end to check
-                    if ((cs & 15u) == 0) {
-#pragma unroll
-                        for (int u = 0; u < U; u += 4) {
-                            const uint4 c4 = lds_u128(cs + 4u * u);
-                            const uint4 a4 = lds_u128(vs + 4u * u);
-                            cu[u] = c4.x; cu[u + 1] = c4.y; cu[u + 2] = c4.z; cu[u + 3] = c4.w;
-                            au[u] = a4.x; au[u + 1] = a4.y; au[u + 2] = a4.z; au[u + 3] = a4.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            cu[u] = lds_u32(cs + 4u * u);
-                            au[u] = lds_u32(vs + 4u * u);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) gather_full(bv[u], (int)cu[u]);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) accs[u % NA].mac(from_bits<T>(au[u]), bv[u]);
-                    dirty = true;
-                    q += U;
-                    continue;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    cu[u] = lds_pred(cs + 4u * u, u < cnt);
-                    au[u] = lds_pred(vs + 4u * u, u < cnt);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    av[u] = from_bits<T>(au[u]);
-                    gather(bv[u], (int)cu[u], u < cnt);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (u < cnt) {
-                        while (e <= q + u) flush();  // rows ending before nonzero q+u (rows first on ties)
-                        accs[u % NA].mac(av[u], bv[u]);
-                        dirty = true;
-                    }
-                }
-                q += cnt;
-            }
-            while (r < ib) flush();
-          } else {
-            // folded workers (small n): each G-lane group walks its own equal share of the merge path
-            // item by item -- nonzero (gather + FMA) or row end (store C row, reset) -- all groups of
-            // the warp in lock-step (equal item counts), item types predicated instead of branched
-            constexpr int UF = (U < 8) ? U : 8;
-            const int items = d1 - d0;
-            const int steps = __reduce_max_sync(FULL, items);
-            const uint32_t col_s = smem_u32(COL) - 4u * (uint32_t)inf.zbase;
-            const uint32_t val_s = smem_u32(VAL) - 4u * (uint32_t)inf.zbase;
-            for (int t0 = 0; t0 < steps; t0 += UF) {
-                unsigned bv[UF][NV][VEC];
-                unsigned au[UF];
-                bool isn[UF], isr[UF];
-                const int rstart = r;
-#pragma unroll
-                for (int u = 0; u < UF; ++u) {
-                    const bool active = t0 + u < items;
-                    isn[u] = active && (q < e);   // rows first on ties: row r ends before nonzero q if e <= q
-                    isr[u] = active && !isn[u];
-                    const unsigned c = lds_pred(col_s + 4u * (uint32_t)q, isn[u]);
-                    au[u] = lds_pred(val_s + 4u * (uint32_t)q, isn[u]);
-                    gather(bv[u], (int)c, isn[u]);
-                    q += isn[u] ? 1 : 0;
-                    if (isr[u]) {
-                        ++r;
-                        e = (r < m) ? Eb[r] : 0x7fffffff;
-                    }
-                }
-                int rr = rstart;
-#pragma unroll
-                for (int u = 0; u < UF; ++u) {
-                    if (isn[u]) {
-                        acc.mac(from_bits<T>(au[u]), bv[u]);
-                        dirty = true;
-                    }
-                    if (isr[u]) {
-                        store_row(rr, acc, true);
-                        acc.reset();
-                        dirty = false;
-                        ++rr;
-                    }
-                }
-            }
-          }
-            collapse();
-
-            // ---- carry resolution (Alg. 1 line 22): sums worker partials of the same row in ascending
-            // worker order; rows whose end item lies in this sub-tile were already written by their
-            // owner and get the sum added (RMW); the sub-tile's open row `re` is returned in `open`.
-            auto resolve = [&](const T* slots, const int* srow, const int* sflag, T (&open)[4], bool& open_any) {
-                open_any = false;
-#pragma unroll
-                for (int t2 = 0; t2 < 4; ++t2) open[t2] = R::id();
-                int w = 0;
-                while (w < NWK) {
-                    const int row = srow[w];
-                    bool any = false;
-                    T sacc[4];
-#pragma unroll
-                    for (int t2 = 0; t2 < 4; ++t2) sacc[t2] = R::id();
-                    int w2 = w;
-                    while (w2 < NWK && srow[w2] == row) {
-                        if (sflag[w2]) {
-                            any = true;
-#pragma unroll
-                            for (int t2 = 0; t2 < 4; ++t2) {
-                                const int cc = lane + 32 * t2;
-                                if (cc < n) sacc[t2] = R::add(sacc[t2], slots[w2 * n + cc]);
-                            }
-                        }
-                        ++w2;
-                    }
-                    if (row == re) {
-                        open_any = any;
-#pragma unroll
-                        for (int t2 = 0; t2 < 4; ++t2) open[t2] = sacc[t2];
-                    } else if (any && row < m) {
-                        T* crow = static_cast<T*>(P.C) + (long long)row * P.ldc;
-#pragma unroll
-                        for (int t2 = 0; t2 < 4; ++t2) {
-                            const int cc = lane + 32 * t2;
-                            if (cc < n) crow[cc] = R::add(__ldcg(crow + cc), sacc[t2]);
-                        }
-                    }
-                    w = w2;
-                }
-            };
-            auto write_global_carry = [&](const T (&open)[4], bool open_any) {
-                const int row = (re < m) ? re : -1;
-                const bool any = (row >= 0) && open_any;
-                if (lane == 0) { P.carry_row[inf.range] = row; P.carry_flag[inf.range] = any ? 1 : 0; }
-                if (any) {
-                    T* cv = static_cast<T*>(P.carry_val) + (long long)inf.range * n;
-#pragma unroll
-                    for (int t2 = 0; t2 < 4; ++t2) {
-                        const int cc = lane + 32 * t2;
-                        if (cc < n) cv[cc] = open[t2];
-                    }
-                }
-            };
-            auto publish = [&](T* slots, int* srow, int* sflag) {
-                if (gl == 0) { srow[wid] = ib; sflag[wid] = dirty ? 1 : 0; }
-                if (dirty) {
-#pragma unroll
-                    for (int v = 0; v < NV; ++v)
-#pragma unroll
-                        for (int x = 0; x < VEC; ++x) {
-                            const int cc = cofs[v] + x;
-                            if (colok[v] && cc < n) slots[wid * n + cc] = acc.v[v][x];
-                        }
-                }
-            };
-
-            if ((inf.flags & 3) == 3) {
-                // whole range in one tile (2-D merge path): barrier-free -- the last worker to finish
-                // resolves the carries, the others move straight on to their next tile
-                T* slots = CwS + (size_t)b * NWK * n;
-                int* srow = CrowS + b * NWK;
-                int* sflag = CflagS + b * NWK;
-                publish(slots, srow, sflag);
-                // hand-off: __syncwarp orders the warp's slot writes before lane 0's acq_rel atomic
-                // (release); the warp whose increment completes the count acquires every earlier
-                // release and passes the ordering on to its lanes with __syncwarp
-                __syncwarp();
-                int last = 0;
-                if (lane == 0) last = (smem_atom_add_acq_rel(&Ccnt[b], 1) == TE_CWARPS - 1) ? 1 : 0;
-                last = __shfl_sync(FULL, last, 0);
-                if (last) {
-                    __syncwarp();
-                    T open[4];
-                    bool open_any;
-                    resolve(slots, srow, sflag, open, open_any);
-                    write_global_carry(open, open_any);
-                    __syncwarp();
-                    if (lane == 0) Ccnt[b] = 0;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[b]);  // buffer and slots of stage b are free
-                continue;
-            }
-
-            // range split over several sub-tiles (1-D nonzero split with many rows): synchronous
-            // resolution with a carry forwarded to the next sub-tile's first worker
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[b]);  // done reading this buffer
-            publish(Cw, Crow, Cflag);
-            named_bar_sync(1, TE_CONSUMERS);
-            if (warp == 0) {
-                T open[4];
-                bool open_any;
-                resolve(Cw, Crow, Cflag, open, open_any);
-                __syncwarp();
-                if (lane == 0) { Crow[NWK] = re; Cflag[NWK] = open_any ? 1 : 0; }
-                if (open_any) {
-#pragma unroll
-                    for (int t2 = 0; t2 < 4; ++t2) {
-                        const int cc = lane + 32 * t2;
-                        if (cc < n) Cw[NWK * n + cc] = open[t2];
-                    }
-                }
-                if (inf.flags & 2) write_global_carry(open, open_any);
-            }
-            named_bar_sync(1, TE_CONSUMERS);
         }
     }
 }
 
 template <typename T, int SR, int MODE, int VEC, int G, int NV, int U>
-__global__ void __launch_bounds__(TE_THREADS, MODE == MODE_MERGE ? TE_MINB_MG : TE_MINB) k_tile(const TileParams P) {
-    tile_body<T, SR, MODE, VEC, G, NV, U, false>(P);
-}
-
-#ifndef RSP_MAXREG
-#define RSP_MAXREG 96  // 9 warps per CTA land 5/4 per SMSP: 2 CTAs per SM need <= 96 registers (64K per SMSP quarter)
-#endif
-template <typename T, int SR, int VEC, int G, int NV, int U>
-__global__ void __maxnreg__(RSP_MAXREG) k_tile_pair(const TileParams P) {
-    tile_body<T, SR, MODE_ROWSPLIT, VEC, G, NV, U, true>(P);
+__global__ void __launch_bounds__(TE_THREADS, TE_MINB) k_tile(const TileParams P) {
+    tile_body<T, SR, MODE, VEC, G, NV, U>(P);
 }
 
 }  // namespace spmm

@@ -31,8 +31,6 @@ SPMM_PLUS_TIMES, SPMM_MIN_PLUS = 0, 1
 SPMM_FLAG_VALIDATE = 1
 SPMM_POLICY_AUTO, SPMM_POLICY_PAPER = 0, 1
 SPMM_PARTITION_MERGE_PATH, SPMM_PARTITION_NONZERO_SPLIT = 0, 1
-SPMM_PAIRING_AUTO, SPMM_PAIRING_OFF, SPMM_PAIRING_ON = 0, 1, 2
-PAIRINGS = {"auto": SPMM_PAIRING_AUTO, "off": SPMM_PAIRING_OFF, "on": SPMM_PAIRING_ON}
 
 ALGOS = {"auto": SPMM_ALGO_AUTO, "rowsplit": SPMM_ALGO_ROWSPLIT, "merge": SPMM_ALGO_MERGE}
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
@@ -45,7 +43,7 @@ EXPORTED = ("spmm_csr_create", "spmm_csr_plan", "spmm_csr_plan_ex", "spmm_csr_ex
 
 class spmm_plan_opts(Structure):
     _fields_ = [("policy", c_int32), ("partition", c_int32), ("items_per_cta", c_int32),
-                ("row_pairing", c_int32), ("reserved", c_int32 * 4)]
+                ("reserved0", c_int32), ("reserved", c_int32 * 4)]
 
 
 class spmm_plan_info(Structure):
@@ -53,7 +51,7 @@ class spmm_plan_info(Structure):
                 ("semiring", c_int32), ("dtype", c_int32), ("policy", c_int32), ("partition", c_int32),
                 ("mean_row_length", c_double), ("max_row_length", c_int64), ("threshold", c_double),
                 ("num_ctas", c_int32), ("items_per_cta", c_int32), ("launches_per_execute", c_int32),
-                ("row_pairing", c_int32), ("workspace_bytes", c_size_t), ("b_staging", c_int32),
+                ("compute_launch", c_int32), ("workspace_bytes", c_size_t), ("b_staging", c_int32),
                 ("rows_per_tile", c_int32), ("bspan_compact", c_double)]
 
 
@@ -139,9 +137,8 @@ def spmm_csr_plan(h, n, algo, semiring, threshold=0.0, stream=None):
     return st, ws.value, chosen.value
 
 
-def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None,
-                     row_pairing=0):
-    o = spmm_plan_opts(policy, partition, items_per_cta, row_pairing)
+def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None):
+    o = spmm_plan_opts(policy, partition, items_per_cta, 0)
     ws = c_size_t(0)
     chosen = c_int32(0)
     st = load().spmm_csr_plan_ex(h, n, algo, semiring, threshold, ctypes.byref(o), stream, ctypes.byref(ws),
@@ -200,7 +197,11 @@ def _dtype_code(t) -> int:
 
 
 class CsrSpmm:
-    """C = A (x) B for a CSR matrix A held in torch CUDA tensors (borrowed, never copied)."""
+    """C = A (x) B for a CSR matrix A held in torch CUDA tensors (borrowed, never copied).
+
+    One workspace per plan: executes of one CsrSpmm must not overlap on different streams (they share
+    the merge kernel's partition / carry arrays and the row-split tile queue).  Use one CsrSpmm per
+    stream for concurrent executes."""
 
     def __init__(self, row_offsets, col_indices, values, k: int, validate: bool = False, stream=None):
         import torch
@@ -228,14 +229,13 @@ class CsrSpmm:
         self.chosen = None
 
     def plan(self, n: int, algo: str = "auto", semiring: str = "plus_times", threshold: float = 0.0,
-             policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None,
-             row_pairing: str = "auto") -> str:
+             policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None) -> str:
         import torch
         st, ws, chosen = spmm_csr_plan_ex(self._h, n, ALGOS[algo], SEMIRINGS[semiring], threshold,
                                           {"auto": SPMM_POLICY_AUTO, "paper": SPMM_POLICY_PAPER}[policy],
                                           {"merge_path": SPMM_PARTITION_MERGE_PATH,
                                            "nonzero_split": SPMM_PARTITION_NONZERO_SPLIT}[partition],
-                                          items_per_cta, _stream_ptr(stream), PAIRINGS[row_pairing])
+                                          items_per_cta, _stream_ptr(stream))
         _check(st, self._h)
         self.n = n
         self.workspace = torch.empty(max(ws, 16), dtype=torch.uint8, device=self.row_offsets.device)
@@ -249,17 +249,28 @@ class CsrSpmm:
         return {f: getattr(inf, f) for f, _ in spmm_plan_info._fields_}
 
     def execute(self, B, C=None, stream=None):
+        """C[:m, :n] = A (x) B.  B: k' x ldb row-major CUDA tensor with k' >= k rows and >= n columns
+        (only columns [0, n) are read); C (optional): m x >= n row-major, overwritten in [0, n)."""
         import torch
         if self.n is None:
             raise RuntimeError("plan() first")
+        dev = self.row_offsets.device
         if not B.is_cuda or B.dim() != 2 or B.stride(1) != 1:
             raise ValueError("B must be a 2-D CUDA tensor with unit column stride (row-major)")
+        if B.device != dev:
+            raise ValueError(f"B is on {B.device}, A on {dev}")
         if B.dtype != self.values.dtype:
             raise TypeError("B dtype must match values")
+        if B.shape[0] < self.k or B.shape[1] < self.n:
+            raise ValueError(f"B is {tuple(B.shape)}, needs at least {self.k} x {self.n}")
         if C is None:
-            C = torch.empty(self.m, self.n, dtype=B.dtype, device=B.device)
+            C = torch.empty(self.m, self.n, dtype=B.dtype, device=dev)
         if C.dim() != 2 or C.stride(1) != 1 or C.dtype != B.dtype:
             raise ValueError("C must be a 2-D row-major tensor of B's dtype")
+        if C.device != dev:
+            raise ValueError(f"C is on {C.device}, A on {dev}")
+        if C.shape[0] != self.m or C.shape[1] < self.n:
+            raise ValueError(f"C is {tuple(C.shape)}, needs {self.m} rows and at least {self.n} columns")
         ldb = B.stride(0) if B.shape[0] > 1 else max(B.shape[1], self.n)
         ldc = C.stride(0) if C.shape[0] > 1 else max(C.shape[1], self.n)
         st = spmm_csr_execute(self._h, c_void_p(B.data_ptr()), ldb, c_void_p(C.data_ptr()), ldc, self.n,

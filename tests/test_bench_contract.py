@@ -35,7 +35,7 @@ def test_cuda_arm_json_line():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    d = _run(["--config", "1", "--steps", "5", "--warmup", "3", "--cpu-budget", "1"])
+    d = _run(["--config", "1", "--steps", "5", "--warmup", "3", "--cpu-budget", "1", "--no-extras"])
     assert BASE_KEYS <= set(d) | {"roofline", "gpu_launches", "clocks"}
     assert {"roofline", "gpu_launches", "clocks"} <= set(d)
     r = d["roofline"]
@@ -46,6 +46,21 @@ def test_cuda_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     assert d["config"]["algo"] == "rowsplit" and d["config"]["l2"].startswith("flushed")
     assert d["dtype"] == "f32" and d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
+    assert d["plan_ms"] > 0 and d["cpu_baseline"]["physical_cores"] >= 1
+    assert 0 < r["ceiling"]["frac_ceiling"] <= 1.0
+
+
+@pytest.mark.gpu
+def test_cuda_arm_merge_config_and_extras():
+    """R-MAT 22 as the head (merge: partition + compute + fix-up per step) plus the configs[1] key."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    d = _run(["--config", "2", "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"])
+    assert d["config"]["algo"] == "merge" and d["gpu_launches"] == 4 * 3
+    assert d["roofline"]["kernel"] == "k_merge_w" and d["scaling"] == "strong"
+    assert "config1" in d and d["config1"]["algo"] == "rowsplit" and d["config1"]["value"] > 0
+    assert d["config1"]["roofline"]["frac"] > 0
 
 
 @pytest.mark.gpu

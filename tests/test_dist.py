@@ -25,13 +25,30 @@ def _free_port():
 
 
 def _oracle_local(kind):
-    def fn(ro, col, val, B, k, n, algo="auto", semiring="plus_times"):
-        m = ro.numel() - 1
-        out = oracle.spmm(kind, m, k, n, ro, col, val, B)
-        if kind == "f32_plus_times":
-            return torch.from_numpy(out[0].astype(np.float32))
-        return torch.from_numpy(out)
-    return fn
+    """Per-rank SpMM stand-in for the CPU tests: the oracle behind the RowBlockSpmm local interface."""
+    class OracleLocal:
+        def __init__(self, ro, col, val, k):
+            self.ro, self.col, self.val, self.k = ro, col, val, k
+
+        def plan(self, n, algo="auto", semiring="plus_times", **kw):
+            self.n = n
+            return algo
+
+        def execute(self, B, C=None):
+            m = self.ro.numel() - 1
+            out = oracle.spmm(kind, m, self.k, self.n, self.ro, self.col, self.val, B)
+            out = torch.from_numpy(out[0].astype(np.float32) if kind == "f32_plus_times" else out)
+            if C is not None:
+                C.copy_(out)
+                return C
+            return out
+
+        def info(self):
+            return {}
+
+        def close(self):
+            pass
+    return OracleLocal
 
 
 def _worker(rank, world, port, kind, mode, q):
@@ -44,10 +61,10 @@ def _worker(rank, world, port, kind, mode, q):
         n = 33
         B = synth.dense(p.k, n, 6, kind) if rank == 0 else torch.empty(0)
         C_local, bounds = D.distributed_spmm(p.row_offsets, p.col_indices, val, B, p.k, n, mode=mode,
-                                             gather=False, local_spmm=_oracle_local(kind),
+                                             gather=False, local_factory=_oracle_local(kind),
                                              device=torch.device("cpu"))
         C_full, bounds2 = D.distributed_spmm(p.row_offsets, p.col_indices, val, B, p.k, n, mode=mode,
-                                             gather=True, local_spmm=_oracle_local(kind),
+                                             gather=True, local_factory=_oracle_local(kind),
                                              device=torch.device("cpu"))
         q.put((rank, bounds, C_local.numpy(), C_full.numpy()))
     finally:

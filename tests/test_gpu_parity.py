@@ -93,7 +93,7 @@ def test_config0_parity(kind, n, algo):
 
 
 @pytest.mark.parametrize("partition", ["merge_path", "nonzero_split"])
-@pytest.mark.parametrize("items", [256, 512, 2048, 4096])
+@pytest.mark.parametrize("items", [32, 96, 256, 512, 2048, 4096])
 @pytest.mark.parametrize("kind", ["f32_plus_times", "i32_min_plus"])
 def test_merge_partitions_and_tile_sizes(partition, items, kind):
     p = synth.lognormal_rows(3000, 2000, 7.92, 17)  # ragged rows, empty rows, several CTAs
@@ -285,11 +285,20 @@ def test_rowsplit_tile_queue_for_irregular_rows(kind, n):
     # the row tiles from a queue in the workspace (256 bytes); results unchanged
     p = synth.lognormal_rows(20000, 9000, 7.92, 77)
     val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
-    chosen, info = run_gpu(p, kind, n, "auto", ro, ci, vd, Bd, Cd)
-    assert chosen == "rowsplit" and info["workspace_bytes"] == 256
+    sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
+    op = S.CsrSpmm(ro, ci, vd, p.k)
+    assert op.plan(n, "auto", sr) == "rowsplit"
+    info = op.info()
+    assert info["workspace_bytes"] == 256 and info["launches_per_execute"] == 2 and info["compute_launch"] == 1
+    op.execute(Bd, Cd)
+    torch.cuda.synchronize()
     check(p, kind, n, val, Bh, Cd)
-    # executing twice with the same workspace re-zeroes the queue
-    run_gpu(p, kind, n, "auto", ro, ci, vd, Bd, Cd)
+    # a second execute on the SAME op and workspace, C re-poisoned: the queue must be re-zeroed, or
+    # every tile would be skipped and the poison would survive
+    Cd.fill_(float("nan") if kind.startswith("f32") else -(2**31))
+    op.execute(Bd, Cd)
+    torch.cuda.synchronize()
+    op.close()
     check(p, kind, n, val, Bh, Cd)
 
 
@@ -374,75 +383,6 @@ def test_full_size_configs_sampled(cfg, algo):
     check(p, kind, n, val, Bh, Cd, rows=rows)
     # every row was written (no poison left anywhere)
     assert not torch.isnan(Cd).any()
-
-
-# ------------------------------------------------------------------------------------------------
-# row-pair mode of the row-split kernel (spmm_plan_opts.row_pairing)
-# ------------------------------------------------------------------------------------------------
-def _pair_families():
-    fam = {
-        "banded_odd_rows": synth.banded(3001),  # odd row count: the last pair has no second row
-        "banded_wide": synth.banded(2048, lo=20, hi=19),  # 40 nnz/row: longer than 32, plain fallback
-        "banded_narrow": synth.banded(1500, lo=1, hi=1),
-        "uniform": synth.uniform_rows(1000, 700, 16, 41),
-        "lengths_1_31_32_33": family("lengths_1_31_32_33"),
-        "many_empty_rows": family("many_empty_rows"),
-        "unsorted_duplicates": family("unsorted_duplicates"),
-        "rmat12": family("rmat12"),
-        "all_empty": family("all_empty"),
-        "single_row_single_nnz": family("single_row_single_nnz"),
-    }
-    # banded pattern whose odd rows list their partner's columns reversed plus a duplicate (raw CSR,
-    # not canonicalised): pairing must still use every stored entry exactly once
-    cols, ro = [], [0]
-    for i in range(600):
-        base = sorted({(i + o) % 600 for o in range(-4, 5)})
-        cols += base if i % 2 == 0 else base[::-1] + [base[0]]
-        ro.append(len(cols))
-    fam["shuffled_partner"] = synth.CsrPattern(600, 600, torch.tensor(ro, dtype=torch.int32),
-                                               torch.tensor(cols, dtype=torch.int32), "shuffled_partner")
-    return fam
-
-
-_PAIR_FAM = {}
-
-
-@pytest.mark.parametrize("fam", ["banded_odd_rows", "banded_wide", "banded_narrow", "uniform", "lengths_1_31_32_33",
-                                 "many_empty_rows", "unsorted_duplicates", "rmat12", "all_empty",
-                                 "single_row_single_nnz", "shuffled_partner"])
-@pytest.mark.parametrize("kind", synth.KINDS)
-@pytest.mark.parametrize("n", [1, 8, 16, 32, 64, 100, 128])
-def test_row_pairing_parity(fam, kind, n):
-    if not _PAIR_FAM:
-        _PAIR_FAM.update(_pair_families())
-    p = _PAIR_FAM[fam]
-    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
-    chosen, info = run_gpu(p, kind, n, "rowsplit", ro, ci, vd, Bd, Cd, row_pairing="on")
-    assert chosen == "rowsplit" and info["row_pairing"] == 1
-    check(p, kind, n, val, Bh, Cd)
-
-
-def test_row_pairing_bit_identical_in_exact_semirings_and_auto_choice():
-    p = synth.banded(5000)
-    for kind in ("i32_plus_times", "i32_min_plus", "f32_min_plus"):
-        outs = []
-        for pairing in ("on", "off"):
-            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, 64)
-            run_gpu(p, kind, 64, "rowsplit", ro, ci, vd, Bd, Cd, row_pairing=pairing)
-            outs.append(Cd.cpu())
-        assert torch.equal(outs[0], outs[1])
-    # the plan reports the pairing it chose: on when asked for, never under policy PAPER; AUTO keeps
-    # the paper's one row per group on B200 (pairing measured slower)
-    for pat in (synth.banded(5000), synth.uniform_rows(5000, 5000, 16, 3)):
-        vd = synth.values(pat.nnz, 1, "f32_plus_times").to(DEV)
-        op = S.CsrSpmm(pat.row_offsets.to(DEV), pat.col_indices.to(DEV), vd, pat.k)
-        assert op.plan(64, "rowsplit", row_pairing="on") == "rowsplit"
-        assert op.info()["row_pairing"] == 1
-        op.plan(64, "rowsplit", policy="paper")
-        assert op.info()["row_pairing"] == 0
-        op.plan(64, "rowsplit", row_pairing="off")
-        assert op.info()["row_pairing"] == 0
-        op.close()
 
 
 # ------------------------------------------------------------------------------------------------
