@@ -77,15 +77,18 @@ template <typename T, int SR, int VEC, int NV> struct MAcc {
     }
 };
 
+#ifndef MW_LDG_HINT
+#define MW_LDG_HINT ".nc"  // B-row gathers: read-only path
+#endif
 template <int VEC> __device__ __forceinline__ void mw_ldg(unsigned (&o)[VEC], const void* p);
 template <> __device__ __forceinline__ void mw_ldg<1>(unsigned (&o)[1], const void* p) {
-    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(o[0]) : "l"(p));
+    asm volatile("ld.global" MW_LDG_HINT ".b32 %0, [%1];" : "=r"(o[0]) : "l"(p));
 }
 template <> __device__ __forceinline__ void mw_ldg<2>(unsigned (&o)[2], const void* p) {
-    asm volatile("ld.global.nc.v2.b32 {%0, %1}, [%2];" : "=r"(o[0]), "=r"(o[1]) : "l"(p));
+    asm volatile("ld.global" MW_LDG_HINT ".v2.b32 {%0, %1}, [%2];" : "=r"(o[0]), "=r"(o[1]) : "l"(p));
 }
 template <> __device__ __forceinline__ void mw_ldg<4>(unsigned (&o)[4], const void* p) {
-    asm volatile("ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p));
+    asm volatile("ld.global" MW_LDG_HINT ".v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]) : "l"(p));
 }
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
