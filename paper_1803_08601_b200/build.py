@@ -9,14 +9,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libspmm.so")
-SOURCES = [os.path.join(CSRC, "spmm_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "ptx.cuh", "tile.cuh", "merge.cuh", "merge_w.cuh")] + \
-    [os.path.join(ROOT, "include", "spmm.h")]
+# the C ABI / planner, and one kernel-instance translation unit per value type x semiring (compiled in
+# parallel, then linked into one shared library)
+SOURCES = [os.path.join(CSRC, f) for f in ("spmm_api.cu", "inst_f32_plus_times.cu", "inst_f32_min_plus.cu",
+                                           "inst_i32_plus_times.cu", "inst_i32_min_plus.cu")]
+HEADERS = ("common.cuh", "ptx.cuh", "tile.cuh", "merge.cuh", "merge_w.cuh", "kernels.h", "launch_kernels.cuh")
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "spmm.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xcompiler", "-fvisibility=hidden",
 ]
 
@@ -36,15 +39,30 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Build libspmm.so (or a variant at `out` with extra -D defines, for tuning experiments)."""
+    """Build libspmm.so (or a variant at `out` with extra -D defines, for tuning experiments): every
+    translation unit is compiled to an object in parallel, then linked with nvcc -shared."""
+    from concurrent.futures import ThreadPoolExecutor
+    import hashlib
     lib = out or LIB
     if not force and out is None and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", lib + ".tmp", *SOURCES]
-    if verbose:
-        cmd += ["-Xptxas", "-v"]
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    tag = hashlib.sha1(("|".join(defines) + "|" + lib).encode()).hexdigest()[:10]
+    odir = os.path.join(ROOT, "build", "obj_" + tag)
+    os.makedirs(odir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
+    extra = ["-Xptxas", "-v"] if verbose else []
+
+    def compile_one(src):
+        obj = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
+        cmd = [_nvcc(), *NVCC_FLAGS, *dflags, *extra, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    subprocess.check_call([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", lib + ".tmp", *objs])
     os.replace(lib + ".tmp", lib)
     return lib
 

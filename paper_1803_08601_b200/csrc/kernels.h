@@ -1,0 +1,64 @@
+// kernels.h -- host-side interface between the C ABI (spmm_api.cu) and the kernel translation units
+// (inst_*.cu, one per value type x semiring, compiled in parallel): launch configuration types, the
+// compile-time tuning constants of the kernels, and the per-kind launch entry points.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "merge_w.cuh"
+#include "tile.cuh"
+
+#ifndef RS_U
+#define RS_U 8  // row split: B rows gathered back to back per row group
+#endif
+#ifndef MW_U
+#define MW_U 8  // merge: B rows gathered per batch (row of <= 2 values per lane)
+#endif
+#ifndef MW_U4
+#define MW_U4 4  // merge: B rows per batch when a lane holds 3-4 values of a row (n > 64)
+#endif
+#ifndef MW_MINB
+#define MW_MINB 5  // merge: 256-thread CTAs per SM (40 warps, <= 48 registers; 6 x 40 registers spills)
+#endif
+#ifndef MW_MINB4
+#define MW_MINB4 5  // merge, 3-4 values of a row per lane
+#endif
+
+namespace spmm {
+
+constexpr int kNumSMs = 148;
+
+// vector shape of a launch: VEC elements per lane access, G lanes per row group (row split) / per
+// worker slot (merge), NV vector blocks per lane
+struct VecCfg {
+    int vec, G, NV;
+};
+
+inline int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        int v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = kNumSMs;
+        sms = v;
+    }
+    return sms;
+}
+
+// k_tile<ROWSPLIT> for this vector shape (cudaErrorNotSupported if no instance)
+template <typename T, int SR> cudaError_t rowsplit_kernel(VecCfg cfg, const TileParams& P, cudaStream_t st);
+// k_merge_w for this vector shape; M == nullptr: only report resident CTAs per SM in *per_sm_out
+template <typename T, int SR>
+cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out);
+
+#define SPMM_EXTERN_KIND(T, SR)                                                                             \
+    extern template cudaError_t rowsplit_kernel<T, SR>(VecCfg, const TileParams&, cudaStream_t);            \
+    extern template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
+SPMM_EXTERN_KIND(float, SR_PLUS_TIMES)
+SPMM_EXTERN_KIND(float, SR_MIN_PLUS)
+SPMM_EXTERN_KIND(int, SR_PLUS_TIMES)
+SPMM_EXTERN_KIND(int, SR_MIN_PLUS)
+#undef SPMM_EXTERN_KIND
+
+}  // namespace spmm

@@ -12,9 +12,8 @@
 
 #include "../../include/spmm.h"
 #include "common.cuh"
+#include "kernels.h"
 #include "merge.cuh"
-#include "tile.cuh"
-#include "merge_w.cuh"
 
 using namespace spmm;
 
@@ -48,10 +47,6 @@ struct spmm_csr_s {
 
 namespace {
 
-constexpr int kNumSMs = 148;
-#ifndef RS_U
-#define RS_U 8
-#endif
 #ifndef RS_DYN_SKEW
 #define RS_DYN_SKEW 4.0  // row split takes tiles from a queue when (AUTO) max row > RS_DYN_SKEW x mean row
 #endif
@@ -73,20 +68,7 @@ constexpr int kNumSMs = 148;
 #ifndef MG_ITEMS
 #define MG_ITEMS 0  // merge-path items per task; 0 = sized at plan time (about 16 tasks per resident warp)
 #endif
-#ifndef MW_U
-#define MW_U 8  // merge: B rows gathered per batch (row of <= 2 values per lane)
-#endif
-#ifndef MW_U4
-#define MW_U4 4  // merge: B rows per batch when a lane holds 3-4 values of a row (n > 64)
-#endif
-#ifndef MW_MINB
-#define MW_MINB 5  // merge: 256-thread CTAs per SM (40 warps, <= 48 registers; 6 x 40 registers spills)
-#endif
-#ifndef MW_MINB4
-#define MW_MINB4 5  // merge, 3-4 values of a row per lane
-#endif
 constexpr int kDefaultItems = MG_ITEMS;
-constexpr int kRowsplitU = RS_U;
 #ifndef RS_BSTAGE
 #define RS_BSTAGE 1  // row split: stage compact B row spans into shared memory with TMA (plan-time measured)
 #endif
@@ -183,10 +165,6 @@ int pow2ceil(int x) {
     return p;
 }
 
-struct VecCfg {
-    int vec, G, NV;
-};
-
 VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, bool folded) {
     const uintptr_t pb = (uintptr_t)B, pc = (uintptr_t)C;
     int vec = 1;
@@ -216,61 +194,6 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
     return c;
 }
 
-// ------------------------------------------------------------------------------------------------
-// dispatch tables
-// ------------------------------------------------------------------------------------------------
-int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
-    }
-    return sms;
-}
-
-// Kernel attributes are set and the occupancy is queried once per (kernel instance, device, shared
-// memory size) -- not on every execute (host overhead on the launch-bound small configs).
-struct LaunchCache {
-    int dev = -1;
-    size_t smem_set = 0;   // largest dynamic shared memory size set so far on `dev`
-    size_t smem_q = 0;     // shared memory size of the cached occupancy query
-    int per_sm = 0;
-};
-
-template <typename T, int SR, int MODE, int V, int G, int NV, int U>
-cudaError_t launch_tile(TileParams P, cudaStream_t st) {
-    void (*kfn)(const TileParams) = k_tile<T, SR, MODE, V, G, NV, U>;
-    static std::mutex mu;
-    static LaunchCache cache[8];
-    const size_t smem = te_smem_bytes(P.capr, P.capz, (int)sizeof(T), P.stages, P.capb);
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        LaunchCache& c = cache[dev & 7];
-        if (c.dev != dev) c = LaunchCache{dev, 0, 0, 0};
-        if (smem > c.smem_set) {
-            e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            c.smem_set = smem;
-        }
-        if (c.per_sm == 0 || c.smem_q != smem) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.per_sm, kfn, TE_THREADS, smem);
-            if (e != cudaSuccess) { c.per_sm = 0; return e; }
-            c.smem_q = smem;
-        }
-        per_sm = c.per_sm;
-    }
-    if (per_sm <= 0) return cudaErrorInvalidConfiguration;
-    const long long grid = std::min<long long>(P.num_ranges, (long long)per_sm * num_sms());
-    if (grid <= 0) return cudaSuccess;
-    kfn<<<(unsigned)grid, TE_THREADS, smem, st>>>(P);
-    return cudaGetLastError();
-}
-
 template <typename T, int SR>
 cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaStream_t st) {
     P.num_ranges = (int)((h->m + h->rows_per_tile - 1) / h->rows_per_tile);
@@ -292,73 +215,19 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
     } else {
         P.tile_ctr = nullptr;
     }
-#define RS_CASE(V, G_, NV_) \
-    case (V)*1000 + (G_)*10 + (NV_): e = launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, kRowsplitU>(P, st); break;
-    switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
-        RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 8, 2) RS_CASE(4, 16, 2)
-        RS_CASE(4, 4, 4) RS_CASE(4, 8, 4)
-        RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 8, 2) RS_CASE(2, 16, 2)
-        RS_CASE(2, 32, 2)
-        RS_CASE(1, 1, 1) RS_CASE(1, 2, 1) RS_CASE(1, 4, 1) RS_CASE(1, 8, 1) RS_CASE(1, 8, 2) RS_CASE(1, 16, 2)
-        RS_CASE(1, 32, 2) RS_CASE(1, 32, 3) RS_CASE(1, 32, 4)
-        default: return cudaErrorNotSupported;
-    }
-#undef RS_CASE
+    e = rowsplit_kernel<T, SR>(cfg, P, st);
     mark(h, ev, st);
     return e;
 }
 
-// k_merge_w launch; with M == nullptr only the resident CTAs per SM are returned in *per_sm_out
-// (plan sizes the merge-path tasks from it: one task per resident worker by default)
-template <typename T, int SR, int V, int NV, int U, int MB>
-cudaError_t launch_merge_w(const MergeParams* M, cudaStream_t st, int* per_sm_out = nullptr) {
-    void (*kfn)(const MergeParams) = k_merge_w<T, SR, V, NV, U, MB>;
-    static std::mutex mu;
-    static int per_sm_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    int per_sm;
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        int& c = per_sm_cache[dev & 7];
-        if (c == 0) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kfn, MW_THREADS, 0);
-            if (e != cudaSuccess) { c = 0; return e; }
-        }
-        per_sm = c;
-    }
-    if (per_sm <= 0) return cudaErrorInvalidConfiguration;
-    if (per_sm_out) *per_sm_out = per_sm;
-    if (!M) return cudaSuccess;
-    const long long grid = std::min<long long>((M->num_tasks + MW_THREADS / 32 - 1) / (MW_THREADS / 32),
-                                               (long long)per_sm * num_sms());
-    if (grid <= 0) return cudaSuccess;
-    kfn<<<(unsigned)grid, MW_THREADS, 0, st>>>(*M);
-    return cudaGetLastError();
-}
-
-// dispatch over the k_merge_w instances by vector shape (pick_vec with G = 32)
-template <typename T, int SR>
-cudaError_t dispatch_merge_w(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out) {
-#define MW_CASE(V, NV_, U_, MB_) \
-    case (V)*10 + (NV_): return launch_merge_w<T, SR, V, NV_, U_, MB_>(M, st, per_sm_out);
-    switch (cfg.vec * 10 + cfg.NV) {
-        MW_CASE(4, 1, MW_U4, MW_MINB4) MW_CASE(2, 1, MW_U, MW_MINB) MW_CASE(2, 2, MW_U4, MW_MINB4)
-        MW_CASE(1, 1, MW_U, MW_MINB) MW_CASE(1, 2, MW_U, MW_MINB) MW_CASE(1, 3, MW_U4, MW_MINB4)
-        MW_CASE(1, 4, MW_U4, MW_MINB4)
-        default: return cudaErrorNotSupported;
-    }
-#undef MW_CASE
-}
 
 int merge_w_per_sm(spmm_dtype dt, spmm_semiring sr, VecCfg cfg) {
     int per_sm = 0;
     cudaError_t e;
-    if (dt == SPMM_F32) e = sr == SPMM_PLUS_TIMES ? dispatch_merge_w<float, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
-                                                  : dispatch_merge_w<float, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
-    else e = sr == SPMM_PLUS_TIMES ? dispatch_merge_w<int, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
-                                   : dispatch_merge_w<int, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    if (dt == SPMM_F32) e = sr == SPMM_PLUS_TIMES ? merge_w_launch<float, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                                  : merge_w_launch<float, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    else e = sr == SPMM_PLUS_TIMES ? merge_w_launch<int, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                   : merge_w_launch<int, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
     return e == cudaSuccess ? per_sm : 0;
 }
 
@@ -393,7 +262,7 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     M.carry_row = carry_row;
     M.carry_flag = carry_flag;
     M.carry_val = carry_val;
-    e = dispatch_merge_w<T, SR>(cfg, &M, st, nullptr);
+    e = merge_w_launch<T, SR>(cfg, &M, st, nullptr);
     mark(h, 2, st);
     if (e != cudaSuccess) return e;
     // phase 3: FixCarryOut (Alg. 1 line 24)

@@ -40,9 +40,26 @@ __global__ void gen_idx(int* idx, long long n, int levels, int mode, uint32_t se
     }
 }
 
-template <int U>
+__device__ __forceinline__ uint64_t mkpol(int kind) {
+    uint64_t p = 0;
+    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    else if (kind == 3) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float2 ldg_pol(const float2* a, uint64_t pol) {
+    float2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+
+// POLICY: 0 none; otherwise rows with popcount(idx) <= hot get policy HOTK, the others COLDK
+// (1 evict_last, 2 evict_first, 3 evict_normal)
+template <int U, int HOTK, int COLDK>
 __global__ void __launch_bounds__(256) k_ldg(const int* __restrict__ idx, long long n, const float2* __restrict__ B,
-                                               float2* out) {
+                                               float2* out, int hot) {
+    const uint64_t ph = mkpol(HOTK), pc = mkpol(COLDK);
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -57,7 +74,13 @@ __global__ void __launch_bounds__(256) k_ldg(const int* __restrict__ idx, long l
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int c = __shfl_sync(0xffffffffu, myidx, (u0 + u) & 31);
-                v[u] = (u0 + u < cnt) ? __ldg(B + (long long)c * 32 + lane) : make_float2(0.f, 0.f);
+                if (u0 + u < cnt) {
+                    const float2* a = B + (long long)c * 32 + lane;
+                    if (HOTK == 0) v[u] = __ldg(a);
+                    else v[u] = ldg_pol(a, __popc(c) <= hot ? ph : pc);
+                } else {
+                    v[u] = make_float2(0.f, 0.f);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) { acc.x += v[u].x; acc.y += v[u].y; }
@@ -103,17 +126,31 @@ int main(int argc, char** argv) {
     const double gb = n * 256.0 / 1e9;
     printf("L = %d (B = %.2f GB), %lld gathers of 256 B (%.2f GB requested)\n", levels, rows * 256.0 / 1e9, n, gb);
     const char* names[3] = {"seq", "uniform", "rmat"};
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 3 && argc <= 3; ++mode) {  // argv[3]: policy experiment only
         gen_idx<<<sms * 8, 256>>>(di, n, levels, mode, 1803);
         cudaDeviceSynchronize();
         for (int cps : {2, 3, 4, 5, 6, 8}) {
             const int grid = sms * cps;
-            const float t8 = timeit([&] { k_ldg<8><<<grid, 256>>>(di, n, B, out); });
-            const float t16 = timeit([&] { k_ldg<16><<<grid, 256>>>(di, n, B, out); });
+            const float t8 = timeit([&] { k_ldg<8, 0, 0><<<grid, 256>>>(di, n, B, out, 0); });
+            const float t16 = timeit([&] { k_ldg<16, 0, 0><<<grid, 256>>>(di, n, B, out, 0); });
             printf("%-8s warps/SM=%2d  U=8 %8.3f ms %6.2f TB/s   U=16 %8.3f ms %6.2f TB/s\n", names[mode], cps * 8,
                    t8, gb / t8, t16, gb / t16);
             fflush(stdout);
         }
+    }
+    // L2 priority by popularity (R-MAT marginal: popcount(idx) small = hot), 48 warps/SM, U = 8
+    gen_idx<<<sms * 8, 256>>>(di, n, levels, 2, 1803);
+    cudaDeviceSynchronize();
+    const int grid = sms * 6;
+    for (int h = levels / 5; h <= levels / 5 + 3; ++h) {
+        long long hot_rows = 0, binom = 1;
+        for (int j = 0; j <= h; ++j) { hot_rows += binom; binom = binom * (levels - j) / (j + 1); }
+        const float a = timeit([&] { k_ldg<8, 1, 2><<<grid, 256>>>(di, n, B, out, h); });
+        const float b = timeit([&] { k_ldg<8, 3, 2><<<grid, 256>>>(di, n, B, out, h); });
+        const float c = timeit([&] { k_ldg<8, 1, 3><<<grid, 256>>>(di, n, B, out, h); });
+        printf("rmat hot = popcount <= %d (%lld rows, %.1f MB): last/first %8.3f ms  normal/first %8.3f ms  "
+               "last/normal %8.3f ms\n", h, hot_rows, hot_rows * 256.0 / 1e6, a, b, c);
+        fflush(stdout);
     }
     return 0;
 }
