@@ -43,8 +43,11 @@ extern "C" {
 
 /* ABI history: 2 = round 1; 3 = row pairing removed (the plan option field is reserved), merge
  * items are per warp task, spmm_plan_info.compute_launch added, row split under the AUTO policy may
- * need a 256-byte workspace (tile queue) -- callers must size the workspace from plan(). */
-#define SPMM_ABI_VERSION 3
+ * need a 256-byte workspace (tile queue) -- callers must size the workspace from plan(); 4 = plan
+ * option merge_worker (was reserved0), plan option tasks_per_warp (was reserved[0]) and
+ * spmm_plan_info.merge_worker_lanes / tasks_per_warp (lane-folded merge, task queue),
+ * spmm_csr_execute_ex (accumulate, peer copies of C) and the spmm_ipc_* buffers. */
+#define SPMM_ABI_VERSION 4
 
 typedef struct spmm_csr_s* spmm_csr_t;
 
@@ -66,6 +69,7 @@ enum { SPMM_FLAG_VALIDATE = 1u };                                       /* one c
 
 typedef enum { SPMM_POLICY_AUTO = 0, SPMM_POLICY_PAPER = 1 } spmm_policy;
 typedef enum { SPMM_PARTITION_MERGE_PATH = 0, SPMM_PARTITION_NONZERO_SPLIT = 1 } spmm_partition;
+typedef enum { SPMM_MERGE_WORKER_AUTO = 0, SPMM_MERGE_WORKER_WARP = 1, SPMM_MERGE_WORKER_FOLDED = 2 } spmm_merge_worker;
 
 /* Optional planner knobs (spmm_csr_plan_ex).  Zero-initialised = defaults. */
 typedef struct {
@@ -82,8 +86,17 @@ typedef struct {
     int32_t items_per_cta;   /* merge-path items (rows + nonzeros) per merge task, the partition
                                 granularity of Alg. 1 line 2; 0 = sized at plan time (256..2048, about
                                 16 tasks per resident worker).  Must be a multiple of 32 in [32, 8192]. */
-    int32_t reserved0;       /* must be zero */
-    int32_t reserved[4];     /* must be zero */
+    int32_t merge_worker;    /* spmm_merge_worker: who walks a merge task.  AUTO (0): lane-folded slots
+                                for n <= 16, else a whole warp.  WARP (1): a whole warp with lanes
+                                over B's columns (k_merge_w).  FOLDED (2): the warp split into 32/G
+                                slots of G lanes (G x VEC >= n), each walking its own piece of the
+                                task's merge path (k_merge_f); n <= 16 only (else
+                                plan returns UNSUPPORTED).                                             */
+    int32_t tasks_per_warp;  /* merge: tasks per resident warp when items_per_cta is 0.  0 = default;
+                                1 = one task per warp, walked in a static order; k > 1 = k tasks per
+                                warp taken from a queue in the workspace (zeroed by the partition
+                                kernel) so warps that finish early take more.  At most 64.          */
+    int32_t reserved[3];     /* must be zero */
 } spmm_plan_opts;
 
 /* Read-only description of the current plan (spmm_csr_get_plan_info). */
@@ -106,6 +119,9 @@ typedef struct {
                                 ldb allow 16-byte aligned rows                          */
     int32_t rows_per_tile;   /* row split: rows per tile                                               */
     double bspan_compact;    /* fraction of nonzeros in tiles whose B span is compact (-1: not measured) */
+    int32_t merge_worker_lanes; /* merge: lanes per merge worker (32 = whole warp, G < 32 = lane-folded
+                                   slots, with 16-byte aligned B / C); 0 for row split              */
+    int32_t tasks_per_warp;  /* merge: tasks per resident warp the plan sized (> 1: taken from a queue) */
 } spmm_plan_info;
 
 /*
@@ -159,6 +175,68 @@ SPMM_API spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo_or
  */
 SPMM_API spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Optional epilogue of execute (spmm_csr_execute_ex).  Zero-initialised = plain execute. */
+#define SPMM_MAX_PEERS 7
+typedef struct {
+    int32_t accumulate;       /* 0: C = A (x) B (overwrite).  1: C = C (+) A (x) B -- rows of C are read
+                                 and combined with the product (plus-times: +, min-plus: min); empty
+                                 rows of A leave C unchanged.  Used by the iterative distributed SpMM
+                                 (dist.IterativeRowBlockSpmm: diagonal block first, then the
+                                 off-diagonal block accumulated).           */
+    int32_t num_peers;        /* 0..SPMM_MAX_PEERS: every finished row of C is ALSO stored, with the same
+                                 value, into each peer_C[i] at row (row + peer_row_offset) -- the
+                                 all-gather of C fused into the SpMM (NEXT-1).  peer_C are device
+                                 pointers valid on this device (CUDA IPC / P2P mappings of other
+                                 GPUs' full C, e.g. from spmm_ipc_open), 16-byte aligned, with
+                                 peer_ldc == ldc.  The peer copies are complete when this execute's
+                                 stream work has completed; the caller orders that with the peers
+                                 (e.g. stream sync + process-group barrier).                        */
+    int64_t peer_row_offset;  /* first global row of this C block in the peer Cs (>= 0)              */
+    int64_t peer_ldc;         /* leading dimension of the peer Cs (must equal ldc)                   */
+    void* peer_C[SPMM_MAX_PEERS];
+    int32_t reserved[4];      /* must be zero                                                        */
+} spmm_exec_opts;
+
+/*
+ * spmm_csr_execute_ex -- spmm_csr_execute with the epilogue options above (opts may be NULL).
+ * Errors: INVALID_ARG for accumulate not in {0,1}, num_peers outside [0, 7], peer_ldc != ldc,
+ * negative peer_row_offset, misaligned peer pointers or non-zero reserved fields; NULL_POINTER for a
+ * NULL peer pointer; otherwise as spmm_csr_execute.
+ */
+SPMM_API spmm_status spmm_csr_execute_ex(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
+                                         void* workspace, size_t workspace_bytes, const spmm_exec_opts* opts,
+                                         void* stream);
+
+/*
+ * CUDA IPC buffers for the peer copies of C (NEXT-1).  The handle is SPMM_IPC_HANDLE_BYTES opaque
+ * bytes (a cudaIpcMemHandle_t) that another process on the same node passes to spmm_ipc_open.
+ *   spmm_ipc_alloc: cudaMalloc `bytes` on the current device (*ptr) and export its handle.
+ *   spmm_ipc_free:  free a buffer from spmm_ipc_alloc (after every peer closed it).
+ *   spmm_ipc_open:  map another process's buffer into this one (*ptr, peer access enabled lazily);
+ *                   fails (SPMM_ERR_CUDA) for a handle exported by the calling process itself.
+ *   spmm_ipc_close: unmap a pointer from spmm_ipc_open.
+ */
+/*
+ * spmm_csr_split_columns -- set-up for the iterative distributed SpMM (NEXT-3): split every row of
+ * A (m x ?, CSR, device) into the entries whose column lies in [c0, c1) and the others, keeping
+ * each row's storage order.  Outputs (device, caller-allocated): ro_in[m+1], col_in / val_in (>= nnz
+ * entries; columns rebased to col - c0) and ro_out[m+1], col_out / val_out (>= nnz entries; global
+ * columns).  *nnz_in (host) receives the number of in-range entries (the rest, nnz - *nnz_in, are
+ * in the "out" part).  Synchronises `stream` (one 4-byte read-back).  Values are copied bit for
+ * bit (dtype only names their 4-byte type).  Errors: INVALID_ARG for c1 < c0 or sizes >= 2^31,
+ * NULL_POINTER for missing arrays, CUDA on a runtime error.
+ */
+SPMM_API spmm_status spmm_csr_split_columns(const int32_t* row_offsets, const int32_t* col_indices, const void* values,
+                                            int64_t m, int64_t nnz, int32_t c0, int32_t c1, spmm_dtype dtype,
+                                            int32_t* ro_in, int32_t* col_in, void* val_in, int32_t* ro_out,
+                                            int32_t* col_out, void* val_out, int64_t* nnz_in, void* stream);
+
+#define SPMM_IPC_HANDLE_BYTES 64
+SPMM_API spmm_status spmm_ipc_alloc(size_t bytes, void** ptr, void* handle_out);
+SPMM_API spmm_status spmm_ipc_free(void* ptr);
+SPMM_API spmm_status spmm_ipc_open(const void* handle, void** ptr);
+SPMM_API spmm_status spmm_ipc_close(void* ptr);
 
 /* spmm_csr_destroy -- free the handle (not the borrowed CSR arrays).  NULL is a no-op. */
 SPMM_API spmm_status spmm_csr_destroy(spmm_csr_t h);

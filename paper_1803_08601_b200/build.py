@@ -12,9 +12,9 @@ LIB = os.path.join(HERE, "libspmm.so")
 # the C ABI / planner, and one kernel-instance translation unit per value type x semiring (compiled in
 # parallel, then linked into one shared library)
 SOURCES = [os.path.join(CSRC, f) for f in ("spmm_api.cu", "inst_f32_plus_times.cu", "inst_f32_min_plus.cu",
-                                           "inst_i32_plus_times.cu", "inst_i32_min_plus.cu")]
-HEADERS = ("common.cuh", "ptx.cuh", "tile.cuh", "merge.cuh", "merge_w.cuh", "kernels.h", "launch_kernels.cuh")
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "spmm.h")]
+                                           "inst_i32_plus_times.cu", "inst_i32_min_plus.cu", "csr_split.cu")]
+DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + \
+    [os.path.join(ROOT, "include", "spmm.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

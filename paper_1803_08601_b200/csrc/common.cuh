@@ -92,6 +92,57 @@ template <> __device__ __forceinline__ void st_vec<4>(void* p, const unsigned (&
 }
 
 // ---------------------------------------------------------------------------------------------
+// Epilogue of every finished row of C (spmm_exec_opts): C = C (+) result when accumulating (the
+// diagonal / off-diagonal split of the iterative distributed SpMM), and the
+// same row also stored into up to 7 peer copies of C (the all-gather of C fused into the SpMM, NEXT-1:
+// peer pointers are P2P / IPC mappings of other GPUs' C, so the store travels over NVLink).
+// ---------------------------------------------------------------------------------------------
+constexpr int EPI_MAX_PEERS = 7;
+struct EpiParams {
+    int accumulate;
+    int npeers;
+    long long peer_row0;  // row r of this C is row r + peer_row0 of each peer C
+    long long peer_ldc;
+    void* peer[EPI_MAX_PEERS];
+};
+
+template <int VEC> __device__ __forceinline__ void ld_vec(unsigned (&o)[VEC], const void* p);
+template <> __device__ __forceinline__ void ld_vec<1>(unsigned (&o)[1], const void* p) {
+    o[0] = *reinterpret_cast<const volatile unsigned*>(p);
+}
+template <> __device__ __forceinline__ void ld_vec<2>(unsigned (&o)[2], const void* p) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    o[0] = v.x; o[1] = v.y;
+}
+template <> __device__ __forceinline__ void ld_vec<4>(unsigned (&o)[4], const void* p) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+
+// the epilogue's accumulate / peer path
+template <typename T, int SR, int VEC>
+__device__ __forceinline__ void epi_store_ext(const EpiParams& E, T* p, long long row, int col, unsigned (&o)[VEC]) {
+    if (E.accumulate) {
+        unsigned old[VEC];
+        ld_vec<VEC>(old, p);
+#pragma unroll
+        for (int x = 0; x < VEC; ++x) o[x] = to_bits<T>(Ring<T, SR>::add(from_bits<T>(old[x]), from_bits<T>(o[x])));
+    }
+    st_vec<VEC>(p, o);
+    for (int i = 0; i < E.npeers; ++i)
+        st_vec<VEC>(static_cast<T*>(E.peer[i]) + (row + E.peer_row0) * E.peer_ldc + col, o);
+}
+
+// store VEC values (bit patterns in o) of row `row`, columns [col, col + VEC), through the epilogue
+template <typename T, int SR, int VEC>
+__device__ __forceinline__ void epi_store(const EpiParams& E, T* C, long long ldc, long long row, int col,
+                                          unsigned (&o)[VEC]) {
+    T* p = C + row * ldc + col;
+    if (E.accumulate | E.npeers) epi_store_ext<T, SR, VEC>(E, p, row, col, o);
+    else st_vec<VEC>(p, o);
+}
+
+// ---------------------------------------------------------------------------------------------
 // Warp-cooperative 32-ary search: first x in [lo, hi) with pred(x) true (pred monotone
 // false..true), or hi if none.  ~log32(hi-lo) rounds of one coalesced-ish probe per lane.
 // All 32 lanes must call it with identical arguments.

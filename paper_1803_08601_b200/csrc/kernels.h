@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "merge_f.cuh"
 #include "merge_w.cuh"
 #include "tile.cuh"
 
@@ -20,8 +21,26 @@
 #ifndef MW_MINB
 #define MW_MINB 5  // merge: 256-thread CTAs per SM (40 warps, <= 48 registers; 6 x 40 registers spills)
 #endif
+#ifndef MW_TPW
+#define MW_TPW 1  // merge: tasks per resident warp (1: one static task per warp; > 1: tasks from a queue)
+#endif
+#ifndef MW_TPW_SKEW
+#define MW_TPW_SKEW 8  // merge, AUTO policy, skewed row lengths: tasks per warp, from the queue
+#endif
+#ifndef MF_MAX_N
+#define MF_MAX_N 16  // merge: lane-folded workers (k_merge_f) for n <= MF_MAX_N
+#endif
+#ifndef MF_L
+#define MF_L 8  // merge, folded: items per slot per chunk
+#endif
+#ifndef MF_MINB
+#define MF_MINB 8  // merge, folded: 128-thread CTAs per SM the register allocation targets (VEC = 1)
+#endif
+#ifndef MF_MINB4
+#define MF_MINB4 6  // merge, folded, VEC = 4 (8 gathers x 4 values in flight per lane)
+#endif
 #ifndef MW_MINB4
-#define MW_MINB4 5  // merge, 3-4 values of a row per lane
+#define MW_MINB4 4  // merge, 2-4 values of a row per lane (64 registers: no spills)
 #endif
 
 namespace spmm {
@@ -48,13 +67,17 @@ inline int num_sms() {
 
 // k_tile<ROWSPLIT> for this vector shape (cudaErrorNotSupported if no instance)
 template <typename T, int SR> cudaError_t rowsplit_kernel(VecCfg cfg, const TileParams& P, cudaStream_t st);
-// k_merge_w for this vector shape; M == nullptr: only report resident CTAs per SM in *per_sm_out
+// k_merge_w (cfg.G == 32) / k_merge_f (lane-folded) for this vector shape; M == nullptr: only report
+// the resident warps per SM in *per_sm_out
 template <typename T, int SR>
 cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out);
+template <typename T, int SR>
+cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out);
 
 #define SPMM_EXTERN_KIND(T, SR)                                                                             \
     extern template cudaError_t rowsplit_kernel<T, SR>(VecCfg, const TileParams&, cudaStream_t);            \
-    extern template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
+    extern template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);     \
+    extern template cudaError_t merge_f_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
 SPMM_EXTERN_KIND(float, SR_PLUS_TIMES)
 SPMM_EXTERN_KIND(float, SR_MIN_PLUS)
 SPMM_EXTERN_KIND(int, SR_PLUS_TIMES)

@@ -67,11 +67,11 @@ cudaError_t rowsplit_kernel(VecCfg cfg, const TileParams& P, cudaStream_t st) {
 #undef RS_CASE
 }
 
-// k_merge_w launch; with M == nullptr only the resident CTAs per SM are returned in *per_sm_out
-// (plan sizes the merge-path tasks from it: one task per resident worker by default)
-template <typename T, int SR, int V, int NV, int U, int MB>
-cudaError_t launch_merge_w(const MergeParams* M, cudaStream_t st, int* per_sm_out = nullptr) {
-    void (*kfn)(const MergeParams) = k_merge_w<T, SR, V, NV, U, MB>;
+// launch of a warp-task merge kernel (k_merge_w / k_merge_f): persistent grid of resident CTAs x SMs,
+// capped at one warp per task.  With M == nullptr only the resident CTAs per SM are returned in
+// *per_sm_out (plan sizes the merge-path tasks from it: one task per resident warp by default).
+template <void (*KFN)(const MergeParams), int NT>
+cudaError_t launch_warp_tasks(const MergeParams* M, cudaStream_t st, int* per_sm_out) {
     static std::mutex mu;
     static int per_sm_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int dev = 0;
@@ -82,18 +82,17 @@ cudaError_t launch_merge_w(const MergeParams* M, cudaStream_t st, int* per_sm_ou
         std::lock_guard<std::mutex> lock(mu);
         int& c = per_sm_cache[dev & 7];
         if (c == 0) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, kfn, MW_THREADS, 0);
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, KFN, NT, 0);
             if (e != cudaSuccess) { c = 0; return e; }
         }
         per_sm = c;
     }
     if (per_sm <= 0) return cudaErrorInvalidConfiguration;
-    if (per_sm_out) *per_sm_out = per_sm;
+    if (per_sm_out) *per_sm_out = per_sm * (NT / 32);  // resident warps per SM
     if (!M) return cudaSuccess;
-    const long long grid = std::min<long long>((M->num_tasks + MW_THREADS / 32 - 1) / (MW_THREADS / 32),
-                                               (long long)per_sm * num_sms());
+    const long long grid = std::min<long long>((M->num_tasks + NT / 32 - 1) / (NT / 32), (long long)per_sm * num_sms());
     if (grid <= 0) return cudaSuccess;
-    kfn<<<(unsigned)grid, MW_THREADS, 0, st>>>(*M);
+    KFN<<<(unsigned)grid, NT, 0, st>>>(*M);
     return cudaGetLastError();
 }
 
@@ -101,18 +100,38 @@ cudaError_t launch_merge_w(const MergeParams* M, cudaStream_t st, int* per_sm_ou
 template <typename T, int SR>
 cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out) {
 #define MW_CASE(V, NV_, U_, MB_) \
-    case (V)*10 + (NV_): return launch_merge_w<T, SR, V, NV_, U_, MB_>(M, st, per_sm_out);
+    case (V)*10 + (NV_):                                                                                   \
+        return epi ? launch_warp_tasks<k_merge_w<T, SR, V, NV_, U_, MB_, true>, MW_THREADS>(M, st, per_sm_out)  \
+                   : launch_warp_tasks<k_merge_w<T, SR, V, NV_, U_, MB_, false>, MW_THREADS>(M, st, per_sm_out);
+    const bool epi = M && (M->epi.accumulate || M->epi.npeers);  // epilogue instances only when requested
     switch (cfg.vec * 10 + cfg.NV) {
         MW_CASE(4, 1, MW_U4, MW_MINB4) MW_CASE(2, 1, MW_U, MW_MINB) MW_CASE(2, 2, MW_U4, MW_MINB4)
-        MW_CASE(1, 1, MW_U, MW_MINB) MW_CASE(1, 2, MW_U, MW_MINB) MW_CASE(1, 3, MW_U4, MW_MINB4)
+        MW_CASE(1, 1, MW_U, MW_MINB) MW_CASE(1, 2, MW_U, MW_MINB4) MW_CASE(1, 3, MW_U4, MW_MINB4)
         MW_CASE(1, 4, MW_U4, MW_MINB4)
         default: return cudaErrorNotSupported;
     }
 #undef MW_CASE
 }
 
+// dispatch over the k_merge_f instances (lane-folded merge, n <= MF_MAX_N): VEC in {1, 4}, G lanes per slot
+template <typename T, int SR>
+cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out) {
+#define MF_CASE(V, G_, MB_) \
+    case (V)*100 + (G_):                                                                                   \
+        return epi ? launch_warp_tasks<k_merge_f<T, SR, V, G_, MF_L, MB_, true>, MF_THREADS>(M, st, per_sm_out)  \
+                   : launch_warp_tasks<k_merge_f<T, SR, V, G_, MF_L, MB_, false>, MF_THREADS>(M, st, per_sm_out);
+    const bool epi = M && (M->epi.accumulate || M->epi.npeers);
+    switch (cfg.vec * 100 + cfg.G) {
+        MF_CASE(4, 1, MF_MINB4) MF_CASE(4, 2, MF_MINB4) MF_CASE(4, 4, MF_MINB4)
+        MF_CASE(1, 1, MF_MINB) MF_CASE(1, 2, MF_MINB) MF_CASE(1, 4, MF_MINB) MF_CASE(1, 8, MF_MINB) MF_CASE(1, 16, MF_MINB)
+        default: return cudaErrorNotSupported;
+    }
+#undef MF_CASE
+}
+
 #define SPMM_INSTANTIATE_KIND(T, SR)                                                                        \
     template cudaError_t rowsplit_kernel<T, SR>(VecCfg, const TileParams&, cudaStream_t);                   \
-    template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
+    template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);            \
+    template cudaError_t merge_f_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
 
 }  // namespace spmm

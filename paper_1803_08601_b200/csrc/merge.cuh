@@ -36,8 +36,10 @@ struct NzPred {  // first r with ro[r] > t
 
 // states[2c] = row, states[2c+1] = nonzero, c in [0, num_ctas]
 __global__ void __launch_bounds__(THREADS)
-k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states) {
+k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states,
+            int* __restrict__ task_ctr) {
     const int lane = threadIdx.x & 31;
+    if (task_ctr && blockIdx.x == 0 && threadIdx.x == 0) *task_ctr = 0;  // the compute kernel's task queue
     const long long c = (long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
     if (c > num_ctas) return;
     long long row, nz;
@@ -68,7 +70,7 @@ k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int
 template <typename T, int SR>
 __global__ void __launch_bounds__(THREADS)
 k_fixup(int num_ctas, int n, const int* __restrict__ carry_row, const int* __restrict__ carry_flag,
-        const T* __restrict__ carry_val, T* __restrict__ C, long long ldc) {
+        const T* __restrict__ carry_val, T* __restrict__ C, long long ldc, const EpiParams E) {
     using R = Ring<T, SR>;
     const int lane = threadIdx.x & 31;
     const long long c = (long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
@@ -91,11 +93,17 @@ k_fixup(int num_ctas, int n, const int* __restrict__ carry_row, const int* __res
         }
     }
     if (!any) return;
+    // C[row] (+)= the run (the owner's write, already accumulated into C if requested, came first); the
+    // final row also goes to the peer copies of C
     T* crow = C + (long long)row * ldc;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const int j = lane + 32 * t;
-        if (j < n) crow[j] = R::add(crow[j], s[t]);
+        if (j < n) {
+            const T v = R::add(crow[j], s[t]);
+            crow[j] = v;
+            for (int i = 0; i < E.npeers; ++i) static_cast<T*>(E.peer[i])[(row + E.peer_row0) * E.peer_ldc + j] = v;
+        }
     }
 }
 

@@ -45,7 +45,17 @@ struct MergeParams {
     int* carry_row;
     int* carry_flag;
     void* carry_val;
+    int* task_ctr;  // non-null: warps take tasks from this queue (zeroed by k_partition), else a static
+                    // block of consecutive tasks per warp
+    EpiParams epi;  // accumulate / peer copies of finished rows
 };
+
+// next task of this warp: from the queue (one atomic per task, lane 0) or the next of its static block
+__device__ __forceinline__ int mw_grab(const MergeParams& P) {
+    int t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(P.task_ctr, 1);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
 
 // accumulator of VEC*NV columns for one lane
 template <typename T, int SR, int VEC, int NV> struct MAcc {
@@ -97,7 +107,7 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <typename T, int SR, int VEC, int NV, int U, int MINB>
+template <typename T, int SR, int VEC, int NV, int U, int MINB, bool EPI>
 __global__ void __launch_bounds__(MW_THREADS, MINB) k_merge_w(const MergeParams P) {
     static_assert(32 % U == 0, "a window of 32 nonzeros holds whole batches");
     // per warp: two nonzero windows (column indices | values, filled by cp.async one window ahead) and
@@ -128,14 +138,17 @@ __global__ void __launch_bounds__(MW_THREADS, MINB) k_merge_w(const MergeParams 
 
     // tasks [t0, t1) of this warp, processed in path order: the next task starts where this one ends,
     // so only the end state is loaded per task
+    const bool dyn = P.task_ctr != nullptr;
     const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
     const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int tpw = (P.num_tasks + nwarps - 1) / nwarps;
-    const int t0 = gw * tpw;
-    const int t1 = min(P.num_tasks, t0 + tpw);
-    if (t0 >= t1) return;
-    int r = __ldg(P.states + 2 * t0), q = __ldg(P.states + 2 * t0 + 1);
-    for (int task = t0; task < t1; ++task) {
+    int task = dyn ? mw_grab(P) : gw * tpw;
+    const int t1 = dyn ? P.num_tasks : min(P.num_tasks, gw * tpw + tpw);
+    int r = 0, q = 0;
+    if (task < t1) { r = __ldg(P.states + 2 * task); q = __ldg(P.states + 2 * task + 1); }
+    while (task < t1) {
+        const int next = dyn ? mw_grab(P) : task + 1;  // taken early: the atomic's latency overlaps the task
+        if (dyn) { r = __ldg(P.states + 2 * task); q = __ldg(P.states + 2 * task + 1); }
         const int r1 = __ldg(P.states + 2 * task + 2), q1 = __ldg(P.states + 2 * task + 3);
         // nonzero windows: window w = nonzeros [q_task + 32 w, +32) in slot w & 1
         auto load_window = [&](int zstart, uint32_t slot) {
@@ -163,14 +176,15 @@ __global__ void __launch_bounds__(MW_THREADS, MINB) k_merge_w(const MergeParams 
         bool dirty = false;
 
         auto store_row = [&](int row) {
-            T* crow = static_cast<T*>(P.C) + (long long)row * P.ldc;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 if (colok[v]) {
                     unsigned o[VEC];
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) o[x] = to_bits<T>(acc.v[v][x]);
-                    st_vec<VEC>(crow + cofs[v], o);
+                    T* p = static_cast<T*>(P.C) + (long long)row * P.ldc + cofs[v];
+                    if constexpr (EPI) epi_store_ext<T, SR, VEC>(P.epi, p, row, cofs[v], o);  // accumulate / peers
+                    else st_vec<VEC>(p, o);
                 }
             }
         };
@@ -264,6 +278,7 @@ __global__ void __launch_bounds__(MW_THREADS, MINB) k_merge_w(const MergeParams 
                 }
         }
         __syncwarp();  // the next task reuses the window slots
+        task = next;
     }
 }
 

@@ -37,6 +37,8 @@ struct spmm_csr_s {
     int32_t capz = 4104;          // row split: staged nonzeros per tile (+8 slack)
     int32_t capb = 0;             // row split: bytes of staged B row span per stage (0 = gather B from global)
     bool rs_dyn = false;          // row split: tiles from a queue in the workspace (irregular row lengths)
+    bool mfold = false;           // merge: lane-folded workers (k_merge_f) instead of whole warps (k_merge_w)
+    bool mdyn = false;            // merge: warps take tasks from a queue in the workspace
     double bspan_compact = -1.0;  // fraction of nonzeros in row tiles whose B span is compact (plan-time)
     size_t ws_bytes = 0;
     int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags
@@ -221,13 +223,32 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
 }
 
 
-int merge_w_per_sm(spmm_dtype dt, spmm_semiring sr, VecCfg cfg) {
+// lane-folded merge workers (k_merge_f): VEC = 4 when n, ldb, ldc and the B / C bases allow 16-byte
+// vectors, else 1; G = lanes per slot covering n columns
+VecCfg pick_fold(int n, const void* B, int64_t ldb, const void* C, int64_t ldc) {
+    const uintptr_t pb = (uintptr_t)B, pc = (uintptr_t)C;
+    VecCfg c;
+    c.vec = (n % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && pb % 16 == 0 && pc % 16 == 0) ? 4 : 1;
+    c.G = pow2ceil((n + c.vec - 1) / c.vec);
+    c.NV = 1;
+    return c;
+}
+
+// resident warps per SM of the merge kernel instance used for this shape (0 on error)
+int merge_per_sm_warps(spmm_dtype dt, spmm_semiring sr, VecCfg cfg, bool folded) {
     int per_sm = 0;
     cudaError_t e;
-    if (dt == SPMM_F32) e = sr == SPMM_PLUS_TIMES ? merge_w_launch<float, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
-                                                  : merge_w_launch<float, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
-    else e = sr == SPMM_PLUS_TIMES ? merge_w_launch<int, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
-                                   : merge_w_launch<int, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    if (folded) {
+        if (dt == SPMM_F32) e = sr == SPMM_PLUS_TIMES ? merge_f_launch<float, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                                      : merge_f_launch<float, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+        else e = sr == SPMM_PLUS_TIMES ? merge_f_launch<int, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                       : merge_f_launch<int, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    } else {
+        if (dt == SPMM_F32) e = sr == SPMM_PLUS_TIMES ? merge_w_launch<float, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                                      : merge_w_launch<float, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+        else e = sr == SPMM_PLUS_TIMES ? merge_w_launch<int, SR_PLUS_TIMES>(cfg, nullptr, nullptr, &per_sm)
+                                       : merge_w_launch<int, SR_MIN_PLUS>(cfg, nullptr, nullptr, &per_sm);
+    }
     return e == cudaSuccess ? per_sm : 0;
 }
 
@@ -243,12 +264,13 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     off += align256(sizeof(int) * NC);
     T* carry_val = reinterpret_cast<T*>(ws + off);
     off += align256(sizeof(T) * (size_t)NC * h->n);
+    int* task_ctr = h->mdyn ? reinterpret_cast<int*>(ws + off) : nullptr;  // zeroed by k_partition
     const int items = h->items;
     // phase 1: PartitionSpmm (Alg. 1 line 2)
     const long long pgrid = (NC + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     mark(h, 0, st);
     k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, (int)h->m, (int)h->nnz, items, h->opts.partition, (int)NC,
-                                                     states);
+                                                     states, task_ctr);
     mark(h, 1, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -262,20 +284,22 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     M.carry_row = carry_row;
     M.carry_flag = carry_flag;
     M.carry_val = carry_val;
-    e = merge_w_launch<T, SR>(cfg, &M, st, nullptr);
+    M.task_ctr = task_ctr;
+    M.epi = P.epi;
+    e = h->mfold ? merge_f_launch<T, SR>(cfg, &M, st, nullptr) : merge_w_launch<T, SR>(cfg, &M, st, nullptr);
     mark(h, 2, st);
     if (e != cudaSuccess) return e;
     // phase 3: FixCarryOut (Alg. 1 line 24)
     const long long fgrid = (NC + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     k_fixup<T, SR><<<(unsigned)fgrid, THREADS, 0, st>>>((int)NC, h->n, carry_row, carry_flag, carry_val,
-                                                        static_cast<T*>(P.C), P.ldc);
+                                                        static_cast<T*>(P.C), P.ldc, P.epi);
     mark(h, 3, st);
     return cudaGetLastError();
 }
 
 template <typename T, int SR>
 cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, long long ldc, void* ws,
-                cudaStream_t st) {
+                const EpiParams& epi, cudaStream_t st) {
     TileParams P{};
     P.m = (int)h->m;
     P.n = h->n;
@@ -287,6 +311,7 @@ cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, lo
     P.ldb_bytes = (unsigned)(ldb * (long long)sizeof(T));
     P.C = Cv;
     P.ldc = ldc;
+    P.epi = epi;
 #ifndef PF_OFF
     // L2 prefetch of gathered B rows: needs 16B-aligned rows; prefetch whole 16-byte granules only
     if (((uintptr_t)Bv % 16) == 0 && (P.ldb_bytes % 16) == 0 && h->n * sizeof(T) >= 16)
@@ -296,7 +321,8 @@ cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, lo
         P.tile_ctr = static_cast<int*>(ws);
         return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), P, st);
     }
-    return launch_merge<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, false), P, static_cast<unsigned char*>(ws), st);
+    const VecCfg mc = h->mfold ? pick_fold(h->n, Bv, ldb, Cv, ldc) : pick_vec(h->n, Bv, ldb, Cv, ldc, false);
+    return launch_merge<T, SR>(h, mc, P, static_cast<unsigned char*>(ws), st);
 }
 
 }  // namespace
@@ -415,35 +441,26 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     if (sr != SPMM_PLUS_TIMES && sr != SPMM_MIN_PLUS) return fail(h, SPMM_ERR_INVALID_ARG, "bad semiring");
     spmm_plan_opts o{};
     if (opts) o = *opts;
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i)
         if (o.reserved[i] != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
-    if (o.reserved0 != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
+    if (o.merge_worker < 0 || o.merge_worker > 2) return fail(h, SPMM_ERR_INVALID_ARG, "bad merge_worker");
+    if (o.tasks_per_warp < 0 || o.tasks_per_warp > 64) return fail(h, SPMM_ERR_INVALID_ARG, "tasks_per_warp must be in [0, 64]");
     if (o.policy != SPMM_POLICY_AUTO && o.policy != SPMM_POLICY_PAPER) return fail(h, SPMM_ERR_INVALID_ARG, "bad policy");
     if (o.partition != SPMM_PARTITION_MERGE_PATH && o.partition != SPMM_PARTITION_NONZERO_SPLIT)
         return fail(h, SPMM_ERR_INVALID_ARG, "bad partition");
     int items = o.items_per_cta ? o.items_per_cta : kDefaultItems;
-    if (items == 0 && !(algo == SPMM_ALGO_ROWSPLIT)) {
-        // merge-path items per task (the partition granularity, Alg. 1 line 2): one task per resident
-        // merge worker (warp) of the kernel instance this n uses with aligned B / C, so every worker
-        // streams one contiguous, equal slice of the path and there is one carry-out per worker
-        const VecCfg mc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, false);
-        int per_sm = merge_w_per_sm(h->dtype, sr, mc);
-        if (per_sm <= 0) per_sm = MW_MINB;
-        const long long workers = (long long)num_sms() * per_sm * (MW_THREADS / 32);
-        const long long path = o.partition == SPMM_PARTITION_NONZERO_SPLIT ? h->nnz : h->m + h->nnz;
-        long long it = (path + workers - 1) / workers;
-        it = std::max<long long>(256, (it + 31) / 32 * 32);
-        items = (int)std::min<long long>(it, 1LL << 30);
-    }
-    if (items == 0) items = 256;  // forced row split: unused
-    if (items < 32 || items > (1 << 30) || items % 32 != 0)
+    // merge worker: lane-folded slots for narrow B (Type-2 waste of a whole warp per worker at small n,
+    // PAPER.md:64), else a whole warp over B's columns
+    const bool fold = o.merge_worker == SPMM_MERGE_WORKER_FOLDED ||
+                      (o.merge_worker == SPMM_MERGE_WORKER_AUTO && n <= MF_MAX_N);
+    if (fold && n > 16) return fail(h, SPMM_ERR_UNSUPPORTED, "lane-folded merge workers need n <= 16");
+    if (items != 0 && (items < 32 || items > (1 << 30) || items % 32 != 0))
         return fail(h, SPMM_ERR_INVALID_ARG, "items_per_cta must be a multiple of 32 in [32, 2^30]");
-    o.items_per_cta = items;
     h->threshold = threshold > 0 ? threshold : 9.35;
     h->n = n;
     h->sr = sr;
-    h->opts = o;
-    h->items = items;
+    h->mfold = fold;
+    h->mdyn = false;
     h->max_row = -1;
     h->capb = 0;
     h->bspan_compact = -1.0;
@@ -480,14 +497,48 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     h->ws_bytes = 0;
     h->num_ctas = 0;
     if (pick == SPMM_ALGO_MERGE) {
+        // tasks per warp: AUTO takes tasks from a queue on skewed row lengths (R-MAT: the cost of equal
+        // merge-path slices varies with their B rows' cache behaviour; measured -12% on R-MAT 22), and
+        // one static task per warp otherwise (uniform costs: the queue's smaller tasks only add work)
+        int tpw = o.tasks_per_warp;
+        if (tpw == 0) {
+            tpw = MW_TPW;
+            if (o.policy == SPMM_POLICY_AUTO && h->m > 0) {
+                if (h->max_row < 0) {
+                    const spmm_status ms = measure_max_row(h, stream);
+                    if (ms != SPMM_OK) return ms;
+                }
+                if ((double)h->max_row > 16.0 * d && h->max_row >= 1024) tpw = MW_TPW_SKEW;
+            }
+        }
+        h->mdyn = tpw > 1;
+        if (items == 0) {
+            // merge-path items per task (the partition granularity, Alg. 1 line 2): tpw tasks per
+            // resident merge warp of the kernel instance this n uses with aligned B / C, so every warp
+            // streams contiguous, equal slices of the path
+            const int l4 = n % 4 == 0 ? 4 : 1;
+            const VecCfg mc = fold ? pick_fold(n, nullptr, l4, nullptr, l4) : pick_vec(n, nullptr, l4, nullptr, l4, false);
+            int per_sm = merge_per_sm_warps(h->dtype, sr, mc, fold);
+            if (per_sm <= 0) per_sm = 32;
+            const long long workers = (long long)num_sms() * per_sm * tpw;
+            const long long path = o.partition == SPMM_PARTITION_NONZERO_SPLIT ? h->nnz : h->m + h->nnz;
+            long long it = (path + workers - 1) / workers;
+            it = std::max<long long>(256, (it + 31) / 32 * 32);
+            items = (int)std::min<long long>(it, 1LL << 30);
+        }
+        o.items_per_cta = items;
+        o.tasks_per_warp = tpw;
+        h->items = items;
         const int64_t NC = spmm_merge_num_ctas(h->m, h->nnz, items, o.partition);
         h->num_ctas = NC;
         if (NC > 0) {
             const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
             h->ws_bytes = align256(sizeof(int) * 2 * (NC + 1)) + 2 * align256(sizeof(int) * NC) +
-                          align256(elem * (size_t)NC * n);
+                          align256(elem * (size_t)NC * n) + (h->mdyn ? 256 : 0);
         }
     } else {
+        h->items = items ? items : 256;  // unused by row split
+        o.items_per_cta = h->items;
         // row tiles of R rows sized so a typical tile's nonzeros fit the staged shared-memory slice
         const double dd = std::max(1.0, d);
         int R = 1;
@@ -552,6 +603,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
                     (double)h->max_row > RS_DYN_SKEW * std::max(1.0, d);
         if (h->rs_dyn) h->ws_bytes = 256;
     }
+    h->opts = o;
     h->planned = true;
     if (workspace_bytes) *workspace_bytes = h->ws_bytes;
     if (chosen) *chosen = pick;
@@ -580,16 +632,39 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
     out->b_staging = (h->chosen == SPMM_ALGO_ROWSPLIT && h->capb > 0) ? 1 : 0;
     out->rows_per_tile = h->chosen == SPMM_ALGO_ROWSPLIT ? h->rows_per_tile : 0;
     out->bspan_compact = h->bspan_compact;
+    out->tasks_per_warp = h->chosen == SPMM_ALGO_MERGE ? h->opts.tasks_per_warp : 0;
+    out->merge_worker_lanes = h->chosen == SPMM_ALGO_MERGE ? (h->mfold ? pick_fold(h->n, nullptr, h->n % 4 == 0 ? 4 : 1, nullptr, h->n % 4 == 0 ? 4 : 1).G : 32) : 0;
     out->workspace_bytes = h->ws_bytes;
     return SPMM_OK;
 }
 
-spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
-                             void* workspace, size_t workspace_bytes, void* stream) {
+spmm_status spmm_csr_execute_ex(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
+                                void* workspace, size_t workspace_bytes, const spmm_exec_opts* opts, void* stream) {
     if (!h) return SPMM_ERR_NULL_POINTER;
     if (!h->planned) return fail(h, SPMM_ERR_NOT_PLANNED, "execute before plan");
     if (n != h->n) return fail(h, SPMM_ERR_INVALID_ARG, "n differs from the planned n");
     if (ldb < n || ldc < n) return fail(h, SPMM_ERR_INVALID_ARG, "ldb and ldc must be >= n");
+    EpiParams epi{};
+    if (opts) {
+        for (int i = 0; i < 4; ++i)
+            if (opts->reserved[i] != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved exec option fields must be 0");
+        if (opts->accumulate != 0 && opts->accumulate != 1) return fail(h, SPMM_ERR_INVALID_ARG, "accumulate must be 0 or 1");
+        if (opts->num_peers < 0 || opts->num_peers > SPMM_MAX_PEERS)
+            return fail(h, SPMM_ERR_INVALID_ARG, "num_peers must be in [0, 7]");
+        if (opts->num_peers > 0) {
+            if (opts->peer_ldc != ldc) return fail(h, SPMM_ERR_INVALID_ARG, "peer_ldc must equal ldc");
+            if (opts->peer_row_offset < 0) return fail(h, SPMM_ERR_INVALID_ARG, "peer_row_offset must be >= 0");
+            for (int i = 0; i < opts->num_peers; ++i) {
+                if (!opts->peer_C[i]) return fail(h, SPMM_ERR_NULL_POINTER, "peer_C[i] is NULL");
+                if (((uintptr_t)opts->peer_C[i] % 16) != 0) return fail(h, SPMM_ERR_INVALID_ARG, "peer_C must be 16-byte aligned");
+            }
+        }
+        epi.accumulate = opts->accumulate;
+        epi.npeers = opts->num_peers;
+        epi.peer_row0 = opts->peer_row_offset;
+        epi.peer_ldc = opts->peer_ldc;
+        for (int i = 0; i < opts->num_peers; ++i) epi.peer[i] = opts->peer_C[i];
+    }
     if (h->m == 0) return SPMM_OK;
     if (!C) return fail(h, SPMM_ERR_NULL_POINTER, "C is NULL");
     if (h->nnz > 0 && !B) return fail(h, SPMM_ERR_NULL_POINTER, "B is NULL");
@@ -602,15 +677,63 @@ spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e;
     if (h->dtype == SPMM_F32) {
-        e = (h->sr == SPMM_PLUS_TIMES) ? run<float, SR_PLUS_TIMES>(h, B, ldb, C, ldc, workspace, st)
-                                       : run<float, SR_MIN_PLUS>(h, B, ldb, C, ldc, workspace, st);
+        e = (h->sr == SPMM_PLUS_TIMES) ? run<float, SR_PLUS_TIMES>(h, B, ldb, C, ldc, workspace, epi, st)
+                                       : run<float, SR_MIN_PLUS>(h, B, ldb, C, ldc, workspace, epi, st);
     } else {
-        e = (h->sr == SPMM_PLUS_TIMES) ? run<int, SR_PLUS_TIMES>(h, B, ldb, C, ldc, workspace, st)
-                                       : run<int, SR_MIN_PLUS>(h, B, ldb, C, ldc, workspace, st);
+        e = (h->sr == SPMM_PLUS_TIMES) ? run<int, SR_PLUS_TIMES>(h, B, ldb, C, ldc, workspace, epi, st)
+                                       : run<int, SR_MIN_PLUS>(h, B, ldb, C, ldc, workspace, epi, st);
     }
     if (e == cudaErrorNotSupported) return fail(h, SPMM_ERR_UNSUPPORTED, "no kernel instance for this n / alignment");
     if (e != cudaSuccess) return cuda_fail(h, e, "execute");
     return SPMM_OK;
+}
+
+spmm_status spmm_csr_execute(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+    return spmm_csr_execute_ex(h, B, ldb, C, ldc, n, workspace, workspace_bytes, nullptr, stream);
+}
+
+// ---- device buffers shareable across processes (CUDA IPC), for the peer copies of C (NEXT-1) ----
+static_assert(sizeof(cudaIpcMemHandle_t) == SPMM_IPC_HANDLE_BYTES, "IPC handle size");
+static_assert(SPMM_MAX_PEERS == EPI_MAX_PEERS, "peer count");
+spmm_status spmm_ipc_alloc(size_t bytes, void** ptr, void* handle_out) {
+    if (!ptr || !handle_out) return SPMM_ERR_NULL_POINTER;
+    *ptr = nullptr;
+    if (bytes == 0) return SPMM_ERR_INVALID_ARG;
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return SPMM_ERR_CUDA;
+    cudaIpcMemHandle_t hd;
+    if (cudaIpcGetMemHandle(&hd, p) != cudaSuccess) {
+        cudaFree(p);
+        return SPMM_ERR_CUDA;
+    }
+    std::memcpy(handle_out, &hd, sizeof(hd));
+    *ptr = p;
+    return SPMM_OK;
+}
+
+spmm_status spmm_ipc_free(void* ptr) {
+    if (!ptr) return SPMM_OK;
+    return cudaFree(ptr) == cudaSuccess ? SPMM_OK : SPMM_ERR_CUDA;
+}
+
+spmm_status spmm_ipc_open(const void* handle, void** ptr) {
+    if (!handle || !ptr) return SPMM_ERR_NULL_POINTER;
+    *ptr = nullptr;
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle, sizeof(hd));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return SPMM_ERR_CUDA;
+    }
+    *ptr = p;
+    return SPMM_OK;
+}
+
+spmm_status spmm_ipc_close(void* ptr) {
+    if (!ptr) return SPMM_OK;
+    return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? SPMM_OK : SPMM_ERR_CUDA;
 }
 
 spmm_status spmm_csr_set_timing_events(spmm_csr_t h, void* const* events, int32_t count) {
@@ -631,7 +754,7 @@ spmm_status spmm_merge_partition(const int32_t* row_offsets, int64_t m, int64_t 
     if (num_ctas == 0) return SPMM_OK;
     const long long pgrid = (num_ctas + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     k_partition<<<(unsigned)pgrid, THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        row_offsets, (int)m, (int)nnz, items_per_cta, partition, (int)num_ctas, states_out);
+        row_offsets, (int)m, (int)nnz, items_per_cta, partition, (int)num_ctas, states_out, nullptr);
     return cudaGetLastError() == cudaSuccess ? SPMM_OK : SPMM_ERR_CUDA;
 }
 

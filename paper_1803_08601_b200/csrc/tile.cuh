@@ -49,6 +49,7 @@ struct TileParams {
     int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
     int capb;           // rowsplit: bytes per stage for the tile's B row span (0 = B is gathered from global)
     int* tile_ctr;      // tile queue (irregular rows; zeroed before the launch); null = static round robin
+    EpiParams epi;      // accumulate / peer copies of finished rows
 };
 
 // tile descriptor written by the producer next to the staged data
@@ -403,7 +404,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
     uint32_t boff[NV];  // byte offset of this lane's column block inside a B row (staged B span)
 #pragma unroll
     for (int v = 0; v < NV; ++v) boff[v] = colok[v] ? (uint32_t)(cofs[v] * sizeof(T)) : 0u;
-    T* Cl = static_cast<T*>(P.C) + gl * VEC;
     const unsigned ldb_bytes = P.ldb_bytes;
 
     auto gather = [&](unsigned (&o)[NV][VEC], int c, bool ok) {
@@ -415,14 +415,13 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
         for (int v = 0; v < NV; ++v) ldg_vec<VEC>(o[v], Blv[v] + (size_t)(unsigned)c * ldb_bytes);
     };
     auto store_row = [&](long long row, const Acc<T, SR, VEC, NV>& acc, bool ok) {
-        T* crow = Cl + row * P.ldc;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             if (ok && colok[v]) {
                 unsigned o[VEC];
 #pragma unroll
                 for (int x = 0; x < VEC; ++x) o[x] = to_bits<T>(acc.v[v][x]);
-                st_vec<VEC>(crow + (cofs[v] - gl * VEC), o);
+                epi_store<T, SR, VEC>(P.epi, static_cast<T*>(P.C), P.ldc, row, cofs[v], o);
             }
         }
     };

@@ -31,19 +31,25 @@ SPMM_PLUS_TIMES, SPMM_MIN_PLUS = 0, 1
 SPMM_FLAG_VALIDATE = 1
 SPMM_POLICY_AUTO, SPMM_POLICY_PAPER = 0, 1
 SPMM_PARTITION_MERGE_PATH, SPMM_PARTITION_NONZERO_SPLIT = 0, 1
+SPMM_MERGE_WORKER_AUTO, SPMM_MERGE_WORKER_WARP, SPMM_MERGE_WORKER_FOLDED = 0, 1, 2
+MERGE_WORKERS = {"auto": SPMM_MERGE_WORKER_AUTO, "warp": SPMM_MERGE_WORKER_WARP, "folded": SPMM_MERGE_WORKER_FOLDED}
 
 ALGOS = {"auto": SPMM_ALGO_AUTO, "rowsplit": SPMM_ALGO_ROWSPLIT, "merge": SPMM_ALGO_MERGE}
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 SEMIRINGS = {"plus_times": SPMM_PLUS_TIMES, "min_plus": SPMM_MIN_PLUS}
 
-EXPORTED = ("spmm_csr_create", "spmm_csr_plan", "spmm_csr_plan_ex", "spmm_csr_execute", "spmm_csr_destroy",
-            "spmm_csr_get_plan_info", "spmm_status_string", "spmm_csr_last_error", "spmm_abi_version",
-            "spmm_merge_num_ctas", "spmm_merge_partition", "spmm_partition_rows", "spmm_csr_set_timing_events")
+EXPORTED = ("spmm_csr_create", "spmm_csr_plan", "spmm_csr_plan_ex", "spmm_csr_execute", "spmm_csr_execute_ex",
+            "spmm_csr_destroy", "spmm_csr_get_plan_info", "spmm_status_string", "spmm_csr_last_error",
+            "spmm_abi_version", "spmm_merge_num_ctas", "spmm_merge_partition", "spmm_partition_rows",
+            "spmm_csr_set_timing_events", "spmm_csr_split_columns", "spmm_ipc_alloc", "spmm_ipc_free",
+            "spmm_ipc_open", "spmm_ipc_close")
+SPMM_MAX_PEERS = 7
+SPMM_IPC_HANDLE_BYTES = 64
 
 
 class spmm_plan_opts(Structure):
     _fields_ = [("policy", c_int32), ("partition", c_int32), ("items_per_cta", c_int32),
-                ("reserved0", c_int32), ("reserved", c_int32 * 4)]
+                ("merge_worker", c_int32), ("tasks_per_warp", c_int32), ("reserved", c_int32 * 3)]
 
 
 class spmm_plan_info(Structure):
@@ -52,7 +58,13 @@ class spmm_plan_info(Structure):
                 ("mean_row_length", c_double), ("max_row_length", c_int64), ("threshold", c_double),
                 ("num_ctas", c_int32), ("items_per_cta", c_int32), ("launches_per_execute", c_int32),
                 ("compute_launch", c_int32), ("workspace_bytes", c_size_t), ("b_staging", c_int32),
-                ("rows_per_tile", c_int32), ("bspan_compact", c_double)]
+                ("rows_per_tile", c_int32), ("bspan_compact", c_double), ("merge_worker_lanes", c_int32),
+                ("tasks_per_warp", c_int32)]
+
+
+class spmm_exec_opts(Structure):
+    _fields_ = [("accumulate", c_int32), ("num_peers", c_int32), ("peer_row_offset", c_int64), ("peer_ldc", c_int64),
+                ("peer_C", c_void_p * SPMM_MAX_PEERS), ("reserved", c_int32 * 4)]
 
 
 class SpmmError(RuntimeError):
@@ -83,6 +95,15 @@ def load(path: str | None = None):
                                      c_void_p, POINTER(c_size_t), POINTER(c_int32)]
     lib.spmm_csr_execute.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_size_t,
                                      c_void_p]
+    lib.spmm_csr_execute_ex.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int32, c_void_p, c_size_t,
+                                        POINTER(spmm_exec_opts), c_void_p]
+    lib.spmm_csr_split_columns.argtypes = [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_int32, c_int32,
+                                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                           POINTER(c_int64), c_void_p]
+    lib.spmm_ipc_alloc.argtypes = [c_size_t, POINTER(c_void_p), c_void_p]
+    lib.spmm_ipc_free.argtypes = [c_void_p]
+    lib.spmm_ipc_open.argtypes = [c_void_p, POINTER(c_void_p)]
+    lib.spmm_ipc_close.argtypes = [c_void_p]
     lib.spmm_csr_destroy.argtypes = [c_void_p]
     lib.spmm_csr_get_plan_info.argtypes = [c_void_p, POINTER(spmm_plan_info)]
     lib.spmm_status_string.argtypes = [c_int32]
@@ -137,8 +158,9 @@ def spmm_csr_plan(h, n, algo, semiring, threshold=0.0, stream=None):
     return st, ws.value, chosen.value
 
 
-def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None):
-    o = spmm_plan_opts(policy, partition, items_per_cta, 0)
+def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None,
+                     merge_worker=0, tasks_per_warp=0):
+    o = spmm_plan_opts(policy, partition, items_per_cta, merge_worker, tasks_per_warp)
     ws = c_size_t(0)
     chosen = c_int32(0)
     st = load().spmm_csr_plan_ex(h, n, algo, semiring, threshold, ctypes.byref(o), stream, ctypes.byref(ws),
@@ -148,6 +170,41 @@ def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0,
 
 def spmm_csr_execute(h, B_ptr, ldb, C_ptr, ldc, n, ws_ptr, ws_bytes, stream=None) -> int:
     return load().spmm_csr_execute(h, B_ptr, ldb, C_ptr, ldc, n, ws_ptr, ws_bytes, stream)
+
+
+def spmm_csr_execute_ex(h, B_ptr, ldb, C_ptr, ldc, n, ws_ptr, ws_bytes, opts, stream=None) -> int:
+    return load().spmm_csr_execute_ex(h, B_ptr, ldb, C_ptr, ldc, n, ws_ptr, ws_bytes,
+                                      ctypes.byref(opts) if opts is not None else None, stream)
+
+
+def spmm_csr_split_columns(ro_ptr, col_ptr, val_ptr, m, nnz, c0, c1, dtype, ro_in, col_in, val_in, ro_out, col_out,
+                           val_out, stream=None):
+    nnz_in = c_int64(0)
+    st = load().spmm_csr_split_columns(ro_ptr, col_ptr, val_ptr, m, nnz, c0, c1, dtype, ro_in, col_in, val_in, ro_out,
+                                       col_out, val_out, ctypes.byref(nnz_in), stream)
+    return st, nnz_in.value
+
+
+def spmm_ipc_alloc(nbytes):
+    ptr = c_void_p()
+    handle = ctypes.create_string_buffer(SPMM_IPC_HANDLE_BYTES)
+    st = load().spmm_ipc_alloc(nbytes, ctypes.byref(ptr), handle)
+    return st, ptr.value, handle.raw
+
+
+def spmm_ipc_free(ptr) -> int:
+    return load().spmm_ipc_free(ptr)
+
+
+def spmm_ipc_open(handle: bytes):
+    ptr = c_void_p()
+    buf = ctypes.create_string_buffer(bytes(handle), SPMM_IPC_HANDLE_BYTES)
+    st = load().spmm_ipc_open(buf, ctypes.byref(ptr))
+    return st, ptr.value
+
+
+def spmm_ipc_close(ptr) -> int:
+    return load().spmm_ipc_close(ptr)
 
 
 def spmm_csr_destroy(h) -> int:
@@ -229,13 +286,14 @@ class CsrSpmm:
         self.chosen = None
 
     def plan(self, n: int, algo: str = "auto", semiring: str = "plus_times", threshold: float = 0.0,
-             policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None) -> str:
+             policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None,
+             merge_worker: str = "auto", tasks_per_warp: int = 0) -> str:
         import torch
         st, ws, chosen = spmm_csr_plan_ex(self._h, n, ALGOS[algo], SEMIRINGS[semiring], threshold,
                                           {"auto": SPMM_POLICY_AUTO, "paper": SPMM_POLICY_PAPER}[policy],
                                           {"merge_path": SPMM_PARTITION_MERGE_PATH,
                                            "nonzero_split": SPMM_PARTITION_NONZERO_SPLIT}[partition],
-                                          items_per_cta, _stream_ptr(stream))
+                                          items_per_cta, _stream_ptr(stream), MERGE_WORKERS[merge_worker], tasks_per_warp)
         _check(st, self._h)
         self.n = n
         self.workspace = torch.empty(max(ws, 16), dtype=torch.uint8, device=self.row_offsets.device)
@@ -248,9 +306,12 @@ class CsrSpmm:
         _check(st, self._h)
         return {f: getattr(inf, f) for f, _ in spmm_plan_info._fields_}
 
-    def execute(self, B, C=None, stream=None):
+    def execute(self, B, C=None, stream=None, accumulate: bool = False, peers=None, peer_row_offset: int = 0):
         """C[:m, :n] = A (x) B.  B: k' x ldb row-major CUDA tensor with k' >= k rows and >= n columns
-        (only columns [0, n) are read); C (optional): m x >= n row-major, overwritten in [0, n)."""
+        (only columns [0, n) are read); C (optional): m x >= n row-major, overwritten in [0, n).
+        accumulate=True: C = C (+) A (x) B.  peers: device pointers (ints) of up to 7 other copies of
+        C with the same leading dimension; every finished row r is also stored at row
+        r + peer_row_offset of each (spmm_csr_execute_ex)."""
         import torch
         if self.n is None:
             raise RuntimeError("plan() first")
@@ -273,8 +334,23 @@ class CsrSpmm:
             raise ValueError(f"C is {tuple(C.shape)}, needs {self.m} rows and at least {self.n} columns")
         ldb = B.stride(0) if B.shape[0] > 1 else max(B.shape[1], self.n)
         ldc = C.stride(0) if C.shape[0] > 1 else max(C.shape[1], self.n)
-        st = spmm_csr_execute(self._h, c_void_p(B.data_ptr()), ldb, c_void_p(C.data_ptr()), ldc, self.n,
-                              c_void_p(self.workspace.data_ptr()), self.workspace.numel(), _stream_ptr(stream))
+        if not accumulate and not peers:
+            st = spmm_csr_execute(self._h, c_void_p(B.data_ptr()), ldb, c_void_p(C.data_ptr()), ldc, self.n,
+                                  c_void_p(self.workspace.data_ptr()), self.workspace.numel(), _stream_ptr(stream))
+        else:
+            peers = list(peers or [])
+            if len(peers) > SPMM_MAX_PEERS:
+                raise ValueError(f"at most {SPMM_MAX_PEERS} peers")
+            o = spmm_exec_opts()
+            o.accumulate = 1 if accumulate else 0
+            o.num_peers = len(peers)
+            o.peer_row_offset = peer_row_offset
+            o.peer_ldc = ldc
+            for i, p in enumerate(peers):
+                o.peer_C[i] = p
+            st = spmm_csr_execute_ex(self._h, c_void_p(B.data_ptr()), ldb, c_void_p(C.data_ptr()), ldc, self.n,
+                                     c_void_p(self.workspace.data_ptr()), self.workspace.numel(), o,
+                                     _stream_ptr(stream))
         _check(st, self._h)
         return C
 

@@ -48,7 +48,7 @@ def test_library_is_sm100a_only(lib):
 
 
 def test_status_strings_and_version(lib):
-    assert S.spmm_abi_version() == 3
+    assert S.spmm_abi_version() == 4
     for s in range(8):
         assert S.spmm_status_string(s).startswith("SPMM_")
     assert "unknown" in S.spmm_status_string(99)

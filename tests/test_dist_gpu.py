@@ -122,3 +122,125 @@ def test_row_blocks_rmat16_both_kernels(algo):
     for r in range(2):
         assert res[r][1] == algo
         _check(kind, res[r][3], ref)
+
+
+# ------------------------------------------------------------------------------------------------
+# NEXT-3: iterative SpMM with row-distributed X (CUDA local, split kernel, accumulate epilogue)
+# NEXT-1: C all-gather fused into the SpMM (peer stores through CUDA IPC mappings)
+# ------------------------------------------------------------------------------------------------
+def _iter_worker(rank, world, port, backend, scale, kind, n, mode, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    kw = {"device_id": dev} if backend == "nccl" else {}
+    dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+    try:
+        from paper_1803_08601_b200 import dist as D
+        p, val, _ = _case(scale, kind, n)
+        X = synth.dense(p.m, n, 3000 + scale, kind)
+        sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
+        op = D.IterativeRowBlockSpmm(p.row_offsets, p.col_indices, val, mode=mode, device=dev)
+        op.plan(n, "auto", sr)
+        r0, r1 = op.bounds[rank], op.bounds[rank + 1]
+        Y1 = op.step(X[r0:r1].to(dev))
+        Y2 = op.step(X[r0:r1].to(dev))  # a second step reuses the gathered-X buffer and both plans
+        torch.cuda.synchronize()
+        q.put((rank, op.bounds, Y1.cpu().numpy(), Y2.cpu().numpy()))
+        op.close()
+    except Exception as e:
+        q.put((rank, None, repr(e), None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("n", [4, 64])
+def test_iterative_row_blocks_cuda_vs_oracle(world, backend, kind, n):
+    scale = 12
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_iter_worker, args=(r, world, port, backend, scale, kind, n, 1, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r, bounds, y1, y2 = q.get(timeout=300)
+        assert bounds is not None, f"rank {r} failed: {y1}"
+        res[r] = (bounds, y1, y2)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p, val, _ = _case(scale, kind, n)
+    X = synth.dense(p.m, n, 3000 + scale, kind)
+    ref = oracle.spmm(kind, p.m, p.k, n, p.row_offsets, p.col_indices, val, X)
+    bounds = res[0][0]
+    for r in range(world):
+        r0, r1 = bounds[r], bounds[r + 1]
+        blk = (ref[0][r0:r1], ref[1][r0:r1]) if kind == "f32_plus_times" else ref[r0:r1]
+        _check(kind, res[r][1], blk)
+        _check(kind, res[r][2], blk)
+
+
+def _fused_worker(rank, world, port, backend, scale, kind, n, mode, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    kw = {"device_id": dev} if backend == "nccl" else {}
+    dist.init_process_group(backend, rank=rank, world_size=world, **kw)
+    try:
+        from paper_1803_08601_b200 import dist as D
+        p, val, B = _case(scale, kind, n)
+        sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
+        op = D.RowBlockSpmm(p.row_offsets, p.col_indices, val, p.k, mode=mode, device=dev)
+        op.plan(n, "auto", sr)
+        Bd = op.broadcast_B(B.to(dev) if rank == 0 else None)
+        Cf = op.enable_fused_gather()
+        Cf.fill_(float("nan") if kind.startswith("f32") else -(2**31))
+        out1 = op.execute_gather(Bd).cpu().numpy()
+        dist.barrier()
+        Cf.fill_(float("nan") if kind.startswith("f32") else -(2**31))  # every call rewrites every row
+        dist.barrier()
+        out2 = op.execute_gather(Bd).cpu().numpy()
+        q.put((rank, op.bounds, out1, out2))
+        op.close()
+    except Exception as e:
+        q.put((rank, None, repr(e), None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("n", [8, 64])
+def test_fused_gather_cuda_vs_oracle(world, backend, kind, n):
+    """Each rank's kernels store its finished C rows into its own full C and, through CUDA IPC
+    mappings, into every other rank's full C (two processes on one GPU here; NVLink peers on a node):
+    after execute_gather every rank holds all of C, equal to the oracle."""
+    scale = 13
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, backend, scale, kind, n, 1, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r, bounds, c1, c2 = q.get(timeout=300)
+        assert bounds is not None, f"rank {r} failed: {c1}"
+        res[r] = (bounds, c1, c2)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    p, val, B = _case(scale, kind, n)
+    ref = oracle.spmm(kind, p.m, p.k, n, p.row_offsets, p.col_indices, val, B)
+    for r in range(world):
+        _check(kind, res[r][1], ref)
+        _check(kind, res[r][2], ref)

@@ -563,3 +563,192 @@ def test_config4_rmat26_sampled_rows():
     C = Cd.cpu().numpy()[rows.numpy()]
     ok, worst, idx = oracle.check_f32(C, Cref, bound, TOL)
     assert ok, f"worst |err|/bound {worst} at {idx}"
+
+
+# ------------------------------------------------------------------------------------------------
+# merge workers: whole warp (k_merge_w) vs lane-folded slots (k_merge_f, n <= 16), static tasks vs
+# the task queue (tasks_per_warp > 1)
+# ------------------------------------------------------------------------------------------------
+def _worker_patterns():
+    return {"rmat12": synth.rmat(12, 16, 99), "lognormal": synth.lognormal_rows(3000, 2000, 7.92, 17),
+            "many_empty_rows": family("many_empty_rows"), "giant_row_plus_singletons": family("giant_row_plus_singletons"),
+            "leading_trailing_empty": family("leading_trailing_empty"), "unsorted_duplicates": family("unsorted_duplicates")}
+
+
+_WP = {}
+
+
+@pytest.mark.parametrize("pat", ["rmat12", "lognormal", "many_empty_rows", "giant_row_plus_singletons",
+                                 "leading_trailing_empty", "unsorted_duplicates"])
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 12, 13, 16])
+@pytest.mark.parametrize("worker,tpw", [("folded", 1), ("folded", 4), ("warp", 4)])
+def test_merge_worker_parity(pat, kind, n, worker, tpw):
+    if not _WP:
+        _WP.update(_worker_patterns())
+    p = _WP[pat]
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    _, info = run_gpu(p, kind, n, "merge", ro, ci, vd, Bd, Cd, merge_worker=worker, tasks_per_warp=tpw)
+    assert (info["merge_worker_lanes"] < 32) == (worker == "folded")
+    check(p, kind, n, val, Bh, Cd)
+
+
+@pytest.mark.parametrize("partition", ["merge_path", "nonzero_split"])
+@pytest.mark.parametrize("items", [32, 96, 256, 2048])
+@pytest.mark.parametrize("kind", ["f32_plus_times", "i32_plus_times", "f32_min_plus"])
+@pytest.mark.parametrize("n", [1, 4, 16])
+def test_folded_merge_partitions_and_task_sizes(partition, items, kind, n):
+    # tasks shorter than a chunk, tasks that cut long rows, both partitions
+    p = synth.lognormal_rows(3000, 2000, 7.92, 17)
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    run_gpu(p, kind, n, "merge", ro, ci, vd, Bd, Cd, partition=partition, items_per_cta=items, merge_worker="folded")
+    check(p, kind, n, val, Bh, Cd)
+
+
+@pytest.mark.parametrize("kind", synth.KINDS)
+def test_folded_merge_padding_and_misalignment(kind):
+    """ldb/ldc padding (poisoned) and a misaligned B base: the folded kernel's scalar path (VEC = 1,
+    G up to 16 lanes per slot)."""
+    p = synth.rmat(11, 8, 41)
+    for n, ldb, ldc, off in ((16, 16, 16, 1), (16, 20, 17, 0), (12, 12, 12, 3), (9, 11, 10, 0), (1, 3, 2, 1),
+                             (8, 8, 8, 2), (4, 4, 4, 1)):
+        val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, ldb=ldb, ldc=ldc, b_offset=off)
+        run_gpu(p, kind, n, "merge", ro, ci, vd, Bd, Cd, merge_worker="folded")
+        check(p, kind, n, val, Bh, Cd)
+
+
+def test_merge_workers_bit_identical_in_exact_semirings():
+    p = synth.rmat(13, 8, 5)
+    for kind in ("i32_plus_times", "i32_min_plus", "f32_min_plus"):
+        for n in (1, 4, 16):
+            outs = []
+            for kw in ({"merge_worker": "warp"}, {"merge_worker": "folded"}, {"merge_worker": "folded", "tasks_per_warp": 8},
+                       {"merge_worker": "folded", "partition": "nonzero_split"}, {"merge_worker": "folded", "items_per_cta": 64}):
+                val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+                run_gpu(p, kind, n, "merge", ro, ci, vd, Bd, Cd, **kw)
+                outs.append(Cd.cpu())
+            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+            run_gpu(p, kind, n, "rowsplit", ro, ci, vd, Bd, Cd)
+            outs.append(Cd.cpu())
+            for o in outs[1:]:
+                assert torch.equal(o, outs[0])
+
+
+@pytest.mark.parametrize("worker", ["warp", "folded"])
+def test_merge_task_queue_rezeroed_every_execute(worker):
+    # tasks from the queue: a second execute on the SAME op and workspace (C re-poisoned) must redo
+    # every task, so the partition kernel must have reset the queue
+    p = synth.rmat(12, 16, 99)
+    kind, n = "f32_plus_times", 8
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    op = S.CsrSpmm(ro, ci, vd, p.k)
+    op.plan(n, "merge", merge_worker=worker, tasks_per_warp=4)
+    for _ in range(2):
+        Cd.fill_(float("nan"))
+        op.execute(Bd, Cd)
+        torch.cuda.synchronize()
+        check(p, kind, n, val, Bh, Cd)
+    op.close()
+
+
+def test_folded_merge_rejects_wide_b():
+    p = synth.uniform_rows(100, 100, 4, 2)
+    vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
+    op = S.CsrSpmm(p.row_offsets.to(DEV), p.col_indices.to(DEV), vd, p.k)
+    with pytest.raises(S.SpmmError) as e:
+        op.plan(17, "merge", merge_worker="folded")
+    assert e.value.status == S.SPMM_ERR_UNSUPPORTED
+    op.close()
+
+
+# ------------------------------------------------------------------------------------------------
+# execute epilogue (spmm_csr_execute_ex): accumulate, peer copies of C; column split (NEXT-1/3 set-up)
+# ------------------------------------------------------------------------------------------------
+def _combine_ref(kind, C0, ref):
+    if kind.endswith("min_plus"):
+        return np.minimum(C0, ref)
+    if kind == "i32_plus_times":
+        return (C0.astype(np.int64) + ref.astype(np.int64)).astype(np.uint32).astype(np.int32)
+    return C0.astype(np.float64) + ref
+
+
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("algo,worker", [("rowsplit", "auto"), ("merge", "warp"), ("merge", "folded")])
+@pytest.mark.parametrize("n", [4, 16, 64])
+def test_execute_accumulate_and_peers(kind, algo, worker, n):
+    if worker == "folded" and n > 16:
+        pytest.skip("folded merge is for n <= 16")
+    p = synth.lognormal_rows(2500, 1800, 7.92, 23)  # ragged rows with empty rows, several tasks
+    val, Bh, ro, ci, vd, Bd, _ = make_inputs(p, kind, n)
+    C0 = synth.dense(p.m, n, 31, kind)
+    Cd = C0.to(DEV).clone()
+    off = 37  # this C is rows [37, 37 + m) of the peer copies
+    peers = [torch.full((p.m + 50, n), -7, dtype=C0.dtype, device=DEV) for _ in range(3)]
+    sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
+    op = S.CsrSpmm(ro, ci, vd, p.k)
+    op.plan(n, algo, sr, merge_worker=worker)
+    op.execute(Bd, Cd, accumulate=True, peers=[t.data_ptr() for t in peers], peer_row_offset=off)
+    torch.cuda.synchronize()
+    op.close()
+    ref = oracle.spmm(kind, p.m, p.k, n, p.row_offsets, p.col_indices, val, Bh)
+    C = Cd.cpu().numpy()
+    if kind == "f32_plus_times":
+        want = _combine_ref(kind, C0.numpy(), ref[0])
+        err = np.abs(C.astype(np.float64) - want)
+        assert (err <= 1e-5 * ref[1] + 2.0 ** -22 * np.abs(want) + 1e-30).all(), float(err.max())
+    else:
+        assert np.array_equal(C, _combine_ref(kind, C0.numpy(), ref))
+    for t in peers:  # the peer copies hold the final rows, bit for bit; rows outside are untouched
+        tc = t.cpu()
+        assert torch.equal(tc[off:off + p.m], Cd.cpu())
+        assert (tc[:off] == -7).all() and (tc[off + p.m:] == -7).all()
+
+
+def test_execute_ex_argument_errors():
+    p = synth.uniform_rows(100, 100, 4, 2)
+    vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
+    op = S.CsrSpmm(p.row_offsets.to(DEV), p.col_indices.to(DEV), vd, p.k)
+    op.plan(8, "merge")
+    B = torch.zeros(100, 8, device=DEV)
+    C = torch.zeros(100, 8, device=DEV)
+    D = torch.zeros(200, 8, device=DEV)
+    args = (op._h, B.data_ptr(), 8, C.data_ptr(), 8, 8, op.workspace.data_ptr(), op.workspace.numel())
+
+    def ex(**f):
+        o = S.spmm_exec_opts()
+        for k, v in f.items():
+            if k == "peer_C":
+                for i, x in enumerate(v):
+                    o.peer_C[i] = x
+            else:
+                setattr(o, k, v)
+        return S.spmm_csr_execute_ex(*args, o)
+    assert ex(accumulate=2) == S.SPMM_ERR_INVALID_ARG
+    assert ex(num_peers=8, peer_ldc=8) == S.SPMM_ERR_INVALID_ARG
+    assert ex(num_peers=1, peer_ldc=9, peer_C=[D.data_ptr()]) == S.SPMM_ERR_INVALID_ARG
+    assert ex(num_peers=1, peer_ldc=8) == S.SPMM_ERR_NULL_POINTER
+    assert ex(num_peers=1, peer_ldc=8, peer_C=[D.data_ptr() + 4]) == S.SPMM_ERR_INVALID_ARG
+    assert ex(num_peers=1, peer_ldc=8, peer_row_offset=-1, peer_C=[D.data_ptr()]) == S.SPMM_ERR_INVALID_ARG
+    assert ex(num_peers=1, peer_ldc=8, peer_row_offset=100, peer_C=[D.data_ptr()]) == S.SPMM_OK
+    torch.cuda.synchronize()
+    assert torch.equal(D[100:].cpu(), C.cpu())
+    op.close()
+
+
+@pytest.mark.parametrize("pat", ["rmat12", "unsorted_duplicates", "all_empty", "lognormal"])
+def test_split_columns_kernel(pat):
+    from paper_1803_08601_b200 import dist as D
+    p = synth.lognormal_rows(3000, 2000, 7.92, 17) if pat == "lognormal" else family(pat)
+    val = synth.values(p.nnz, 3, "i32_plus_times")
+    ro, col = p.row_offsets.numpy(), p.col_indices.numpy()
+    for c0, c1 in ((0, p.k // 3), (p.k // 3, 2 * p.k // 3), (0, p.k), (5, 5)):
+        (ri, ci_, vi), (rx, cx, vx) = D.split_columns_cuda(p.row_offsets.to(DEV), p.col_indices.to(DEV), val.to(DEV),
+                                                           c0, c1)
+        ri, ci_, vi, rx, cx, vx = (t.cpu().numpy() for t in (ri, ci_, vi, rx, cx, vx))
+        vn = val.numpy()
+        for r in range(p.m):
+            c = col[ro[r]:ro[r + 1]]
+            v = vn[ro[r]:ro[r + 1]]
+            ins = (c >= c0) & (c < c1)
+            assert np.array_equal(ci_[ri[r]:ri[r + 1]], c[ins] - c0) and np.array_equal(vi[ri[r]:ri[r + 1]], v[ins])
+            assert np.array_equal(cx[rx[r]:rx[r + 1]], c[~ins]) and np.array_equal(vx[rx[r]:rx[r + 1]], v[~ins])
