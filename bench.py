@@ -341,6 +341,7 @@ def summarize(p, n, balg, chosen, info, step_ms, dom_ms, steps, peak, sha, cfg, 
     dom_avg = sum(dom_ms) / len(dom_ms)
     achieved = balg / (dom_avg / 1e3) / 1e9
     kname = KERNEL_NAMES[chosen]
+    ncu = load_traffic(f"config{cfg}_n{n}|{kname}", sha)
     return {
         "workload": WORKLOADS[cfg], "m": p.m, "k": p.k, "nnz": p.nnz, "n": n, "algo": chosen,
         "mean_row_length": info["mean_row_length"], "max_row_length": info["max_row_length"],
@@ -352,8 +353,11 @@ def summarize(p, n, balg, chosen, info, step_ms, dom_ms, steps, peak, sha, cfg, 
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak[0],
                      "peak_source": peak[1], "unit": "GB/s", "frac": round(achieved / peak[0], 4),
                      "frac_vs_nominal_8000": round(achieved / 8000.0, 4),
-                     "traffic": None, "bytes_alg_per_launch": int(balg), "avg_launch_ms": round(dom_avg, 5),
-                     "ncu": load_traffic(f"config{cfg}_n{n}|{kname}", sha)},
+                     "traffic": ncu.get("dram_bytes") if ncu else None,
+                     "traffic_over_alg": round(ncu["dram_bytes"] / balg, 3) if ncu and ncu.get("dram_bytes") else None,
+                     "dram_gbs_at_traffic": round(ncu["dram_bytes"] / (dom_avg / 1e3) / 1e9, 1)
+                     if ncu and ncu.get("dram_bytes") else None,
+                     "bytes_alg_per_launch": int(balg), "avg_launch_ms": round(dom_avg, 5), "ncu": ncu},
         "launches_per_step": info["launches_per_execute"],
     }
 

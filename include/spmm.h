@@ -62,7 +62,9 @@ typedef enum {
     SPMM_ERR_CUDA = 7                 /* a CUDA runtime call or kernel launch failed                */
 } spmm_status;
 
-typedef enum { SPMM_ALGO_AUTO = 0, SPMM_ALGO_ROWSPLIT = 1, SPMM_ALGO_MERGE = 2 } spmm_algo;
+/* TILED (NEXT-4): A/B tiling for dense-ish rows -- needs n % 4 == 0, 32 <= n <= 128
+ * and column indices non-decreasing within rows (checked at plan: UNSUPPORTED otherwise). */
+typedef enum { SPMM_ALGO_AUTO = 0, SPMM_ALGO_ROWSPLIT = 1, SPMM_ALGO_MERGE = 2, SPMM_ALGO_TILED = 3 } spmm_algo;
 typedef enum { SPMM_F32 = 0, SPMM_I32 = 1 } spmm_dtype;                /* dtype of values, B and C */
 typedef enum { SPMM_PLUS_TIMES = 0, SPMM_MIN_PLUS = 1 } spmm_semiring;
 enum { SPMM_FLAG_VALIDATE = 1u };                                       /* one checking pass at create */

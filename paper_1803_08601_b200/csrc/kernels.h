@@ -8,6 +8,7 @@
 #include "merge_f.cuh"
 #include "merge_w.cuh"
 #include "tile.cuh"
+#include "tiled.cuh"
 
 #ifndef RS_U
 #define RS_U 8  // row split: B rows gathered back to back per row group
@@ -27,6 +28,15 @@
 #ifndef MW_TPW_SKEW
 #define MW_TPW_SKEW 8  // merge, AUTO policy, skewed row lengths: tasks per warp, from the queue
 #endif
+#ifndef TL_MIN_D
+#define TL_MIN_D 1000000000.0  // AUTO picks the tiled kernel from this mean row length (set from the sweep)
+#endif
+#ifndef TL_RPG
+#define TL_RPG 4  // tiled: rows per row group (accumulators held across the whole K loop)
+#endif
+#ifndef MW_MIN_ITEMS_DYN
+#define MW_MIN_ITEMS_DYN 1024  // merge, tasks from the queue: fewest items per task
+#endif
 #ifndef MF_MAX_N
 #define MF_MAX_N 16  // merge: lane-folded workers (k_merge_f) for n <= MF_MAX_N
 #endif
@@ -35,6 +45,15 @@
 #endif
 #ifndef MF_MINB
 #define MF_MINB 8  // merge, folded: 128-thread CTAs per SM the register allocation targets (VEC = 1)
+#endif
+#ifndef MF_L_NARROW
+#define MF_L_NARROW 4  // merge, folded, 1-2 lanes per slot: items per slot per chunk
+#endif
+#ifndef MF_MINB_NARROW
+#define MF_MINB_NARROW 12  // merge, folded, 1-2 lanes per slot: CTAs per SM (48 warps)
+#endif
+#ifndef MF_MINB4_NARROW
+#define MF_MINB4_NARROW 8  // merge, folded, float4, 1-2 lanes per slot (4 values per gather: 64 registers)
 #endif
 #ifndef MF_MINB4
 #define MF_MINB4 6  // merge, folded, VEC = 4 (8 gathers x 4 values in flight per lane)
@@ -73,11 +92,14 @@ template <typename T, int SR>
 cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out);
 template <typename T, int SR>
 cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out);
+// k_tiled (NEXT-4) for row groups of cfg.G lanes x cfg.NV float4 blocks
+template <typename T, int SR> cudaError_t tiled_launch(VecCfg cfg, const TiledParams& P, cudaStream_t st);
 
 #define SPMM_EXTERN_KIND(T, SR)                                                                             \
     extern template cudaError_t rowsplit_kernel<T, SR>(VecCfg, const TileParams&, cudaStream_t);            \
     extern template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);     \
-    extern template cudaError_t merge_f_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
+    extern template cudaError_t merge_f_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);     \
+    extern template cudaError_t tiled_launch<T, SR>(VecCfg, const TiledParams&, cudaStream_t);
 SPMM_EXTERN_KIND(float, SR_PLUS_TIMES)
 SPMM_EXTERN_KIND(float, SR_MIN_PLUS)
 SPMM_EXTERN_KIND(int, SR_PLUS_TIMES)

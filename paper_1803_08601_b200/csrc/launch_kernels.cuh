@@ -116,22 +116,60 @@ cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, in
 // dispatch over the k_merge_f instances (lane-folded merge, n <= MF_MAX_N): VEC in {1, 4}, G lanes per slot
 template <typename T, int SR>
 cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out) {
-#define MF_CASE(V, G_, MB_) \
+#define MF_CASE(V, G_, L_, MB_) \
     case (V)*100 + (G_):                                                                                   \
-        return epi ? launch_warp_tasks<k_merge_f<T, SR, V, G_, MF_L, MB_, true>, MF_THREADS>(M, st, per_sm_out)  \
-                   : launch_warp_tasks<k_merge_f<T, SR, V, G_, MF_L, MB_, false>, MF_THREADS>(M, st, per_sm_out);
+        return epi ? launch_warp_tasks<k_merge_f<T, SR, V, G_, L_, MB_, true>, MF_THREADS>(M, st, per_sm_out)  \
+                   : launch_warp_tasks<k_merge_f<T, SR, V, G_, L_, MB_, false>, MF_THREADS>(M, st, per_sm_out);
     const bool epi = M && (M->epi.accumulate || M->epi.npeers);
+    // 1-2 lanes per slot (n <= 2, or n <= 8 with float4): short chunks (L = 4) and more resident warps;
+    // wider slots: L = 8 (profiles/r02_fold_tuning.txt)
     switch (cfg.vec * 100 + cfg.G) {
-        MF_CASE(4, 1, MF_MINB4) MF_CASE(4, 2, MF_MINB4) MF_CASE(4, 4, MF_MINB4)
-        MF_CASE(1, 1, MF_MINB) MF_CASE(1, 2, MF_MINB) MF_CASE(1, 4, MF_MINB) MF_CASE(1, 8, MF_MINB) MF_CASE(1, 16, MF_MINB)
+        MF_CASE(4, 1, MF_L_NARROW, MF_MINB4_NARROW) MF_CASE(4, 2, MF_L_NARROW, MF_MINB4_NARROW) MF_CASE(4, 4, MF_L, MF_MINB4)
+        MF_CASE(1, 1, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(1, 2, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(1, 4, MF_L, MF_MINB)
+        MF_CASE(1, 8, MF_L, MF_MINB) MF_CASE(1, 16, MF_L, MF_MINB)
         default: return cudaErrorNotSupported;
     }
 #undef MF_CASE
 }
 
+// A/B-tiled kernel (NEXT-4): G lanes x NV float4 blocks per row group, RPG rows per group
+template <typename T, int SR, int G, int NV>
+cudaError_t launch_tiled(const TiledParams& P, cudaStream_t st) {
+    void (*kfn)(const TiledParams) = k_tiled<T, SR, G, NV, TL_RPG>;
+    const size_t smem = 2 * (size_t)P.kb * (size_t)P.n * sizeof(T);
+    static std::mutex mu;
+    static size_t smem_set[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (smem > smem_set[dev & 7]) {
+            e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            smem_set[dev & 7] = smem;
+        }
+    }
+    const long long grid = ((long long)P.m + P.rows_per_cta - 1) / P.rows_per_cta;
+    if (grid <= 0) return cudaSuccess;
+    kfn<<<(unsigned)grid, TL_THREADS, smem, st>>>(P);
+    return cudaGetLastError();
+}
+
+template <typename T, int SR>
+cudaError_t tiled_launch(VecCfg cfg, const TiledParams& P, cudaStream_t st) {
+    switch (cfg.G * 10 + cfg.NV) {
+        case 81: return launch_tiled<T, SR, 8, 1>(P, st);
+        case 82: return launch_tiled<T, SR, 8, 2>(P, st);
+        case 162: return launch_tiled<T, SR, 16, 2>(P, st);
+        default: return cudaErrorNotSupported;
+    }
+}
+
 #define SPMM_INSTANTIATE_KIND(T, SR)                                                                        \
     template cudaError_t rowsplit_kernel<T, SR>(VecCfg, const TileParams&, cudaStream_t);                   \
     template cudaError_t merge_w_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);            \
-    template cudaError_t merge_f_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);
+    template cudaError_t merge_f_launch<T, SR>(VecCfg, const MergeParams*, cudaStream_t, int*);            \
+    template cudaError_t tiled_launch<T, SR>(VecCfg, const TiledParams&, cudaStream_t);
 
 }  // namespace spmm

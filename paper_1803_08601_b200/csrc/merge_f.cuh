@@ -31,7 +31,10 @@
 
 namespace spmm {
 
-constexpr int MF_THREADS = 128;  // 4 warps per CTA (the per-warp windows are a few KB each)
+#ifndef MF_THREADS_DEF
+#define MF_THREADS_DEF 128
+#endif
+constexpr int MF_THREADS = MF_THREADS_DEF;  // 4 warps per CTA (the per-warp windows are a few KB each)
 
 template <int VEC> __device__ __forceinline__ void mf_ldg(unsigned (&o)[VEC], const void* p, bool pred);
 template <> __device__ __forceinline__ void mf_ldg<1>(unsigned (&o)[1], const void* p, bool pred) {

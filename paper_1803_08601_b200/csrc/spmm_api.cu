@@ -40,6 +40,8 @@ struct spmm_csr_s {
     bool mfold = false;           // merge: lane-folded workers (k_merge_f) instead of whole warps (k_merge_w)
     bool mdyn = false;            // merge: warps take tasks from a queue in the workspace
     double bspan_compact = -1.0;  // fraction of nonzeros in row tiles whose B span is compact (plan-time)
+    int32_t tl_kb = 0;            // tiled: B rows per shared-memory block
+    int sorted = -1;              // column indices non-decreasing within rows: -1 unknown, 0 no, 1 yes
     size_t ws_bytes = 0;
     int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
@@ -142,6 +144,19 @@ __global__ void k_tile_span(const int* __restrict__ ro, const int* __restrict__ 
     }
 }
 
+// plan-time check, warp per row: column indices non-decreasing within every row (flag = 1 otherwise)
+__global__ void k_check_sorted(const int* __restrict__ ro, const int* __restrict__ col, long long m,
+                               int* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = (long long)gridDim.x * (blockDim.x / 32);
+    int bad = 0;
+    for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / 32; r < m; r += nw) {
+        const int s = ro[r], e = ro[r + 1];
+        for (int q = s + 1 + lane; q < e; q += 32) bad |= (col[q] < col[q - 1]) ? 1 : 0;
+    }
+    if (__any_sync(FULL, bad) && lane == 0) atomicOr(flag, 1);
+}
+
 // flags: bit0 ro[0] != 0, bit1 decreasing offsets, bit2 ro[m] != nnz, bit3 column out of range
 __global__ void k_validate(const int* __restrict__ ro, long long m, long long nnz, const int* __restrict__ col,
                            long long k, int* __restrict__ flags) {
@@ -234,6 +249,14 @@ VecCfg pick_fold(int n, const void* B, int64_t ldb, const void* C, int64_t ldc) 
     return c;
 }
 
+// tiled kernel row groups: float4 over n (n % 4 == 0), G lanes x NV blocks as the row split picks them
+VecCfg tiled_cfg(int n) { return pick_vec(n, nullptr, 4, nullptr, 4, true); }
+bool tiled_shape_ok(int n) {
+    if (n % 4 != 0 || n < 32 || n > 128) return false;
+    const VecCfg c = tiled_cfg(n);
+    return c.vec == 4 && ((c.G == 8 && (c.NV == 1 || c.NV == 2)) || (c.G == 16 && c.NV == 2));
+}
+
 // resident warps per SM of the merge kernel instance used for this shape (0 on error)
 int merge_per_sm_warps(spmm_dtype dt, spmm_semiring sr, VecCfg cfg, bool folded) {
     int per_sm = 0;
@@ -317,6 +340,21 @@ cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, lo
     if (((uintptr_t)Bv % 16) == 0 && (P.ldb_bytes % 16) == 0 && h->n * sizeof(T) >= 16)
         P.pf_bytes = (unsigned)((h->n * sizeof(T)) & ~(size_t)15);
 #endif
+    if (h->chosen == SPMM_ALGO_TILED) {
+        TiledParams Q{};
+        Q.m = P.m; Q.n = P.n; Q.k = (int)h->k; Q.nnz = P.nnz;
+        Q.ro = P.ro; Q.col = P.col; Q.val = P.val;
+        Q.B = Bv; Q.ldb = ldb; Q.C = Cv; Q.ldc = ldc;
+        Q.kb = h->tl_kb;
+        Q.rows_per_cta = h->rows_per_tile;
+        Q.b_vec4 = ((uintptr_t)Bv % 16) == 0 && ldb % 4 == 0;
+        Q.c_vec4 = ((uintptr_t)Cv % 16) == 0 && ldc % 4 == 0;
+        Q.epi = P.epi;
+        mark(h, 0, st);
+        const cudaError_t e = tiled_launch<T, SR>(tiled_cfg(h->n), Q, st);
+        mark(h, 1, st);
+        return e;
+    }
     if (h->chosen == SPMM_ALGO_ROWSPLIT) {
         P.tile_ctr = static_cast<int*>(ws);
         return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), P, st);
@@ -341,6 +379,24 @@ static spmm_status measure_max_row(spmm_csr_t h, void* stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(h, e, "plan: max row length");
     h->max_row = hmax;
+    return SPMM_OK;
+}
+
+// plan-time O(nnz) device check for the tiled kernel: are column indices non-decreasing within rows?
+static spmm_status measure_sorted(spmm_csr_t h, void* stream) {
+    if (h->sorted >= 0) return SPMM_OK;  // A is immutable while the handle lives: checked once
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int flag = 0;
+    cudaError_t e = cudaMemsetAsync(h->d_scratch, 0, sizeof(int), st);
+    if (e == cudaSuccess && h->m > 0) {
+        const int grid = (int)std::min<long long>((h->m * 32 + THREADS - 1) / THREADS, 16LL * kNumSMs);
+        k_check_sorted<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, h->d_scratch);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, h->d_scratch, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "plan: sortedness check");
+    h->sorted = flag ? 0 : 1;
     return SPMM_OK;
 }
 
@@ -436,7 +492,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     h->planned = false;
     if (n < 1) return fail(h, SPMM_ERR_INVALID_ARG, "n must be >= 1");
     if (n > 128) return fail(h, SPMM_ERR_UNSUPPORTED, "n > 128 is not implemented (SURVEY.md §8(b))");
-    if (algo != SPMM_ALGO_AUTO && algo != SPMM_ALGO_ROWSPLIT && algo != SPMM_ALGO_MERGE)
+    if (algo != SPMM_ALGO_AUTO && algo != SPMM_ALGO_ROWSPLIT && algo != SPMM_ALGO_MERGE && algo != SPMM_ALGO_TILED)
         return fail(h, SPMM_ERR_INVALID_ARG, "bad algo");
     if (sr != SPMM_PLUS_TIMES && sr != SPMM_MIN_PLUS) return fail(h, SPMM_ERR_INVALID_ARG, "bad semiring");
     spmm_plan_opts o{};
@@ -491,12 +547,34 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             // profiles/r01_density_sweep.txt), while merge path stages fixed-size slices at any d
             const bool long_rows = RS_ZF / 10.0 * 16.0 * d > (double)(RS_CAPZ_MAX - 8);
             pick = (skewed || few_rows || long_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
+            // dense-ish rows (NEXT-4): B streamed once per row tile beats a B-row gather
+            // per nonzero once d is large (measured crossover)
+            if (d >= TL_MIN_D && !skewed && tiled_shape_ok(n)) {
+                const spmm_status ss = measure_sorted(h, stream);
+                if (ss != SPMM_OK) return ss;
+                if (h->sorted == 1) pick = SPMM_ALGO_TILED;
+            }
         }
+    }
+    if (pick == SPMM_ALGO_TILED) {
+        if (!tiled_shape_ok(n)) return fail(h, SPMM_ERR_UNSUPPORTED, "tiled kernel needs n % 4 == 0 and 32 <= n <= 128");
+        const spmm_status ss = measure_sorted(h, stream);
+        if (ss != SPMM_OK) return ss;
+        if (h->sorted != 1)
+            return fail(h, SPMM_ERR_UNSUPPORTED, "tiled kernel needs column indices non-decreasing within rows");
     }
     h->chosen = pick;
     h->ws_bytes = 0;
     h->num_ctas = 0;
-    if (pick == SPMM_ALGO_MERGE) {
+    if (pick == SPMM_ALGO_TILED) {
+        const VecCfg tc = tiled_cfg(n);
+        const size_t elem = h->dtype == SPMM_F32 ? sizeof(float) : sizeof(int);
+        h->tl_kb = (int)std::max<size_t>(1, TL_BUF_BYTES / ((size_t)n * elem));
+        h->rows_per_tile = (TL_THREADS / 32) * (32 / tc.G) * TL_RPG;
+        h->num_ctas = (h->m + h->rows_per_tile - 1) / h->rows_per_tile;
+        h->items = items ? items : 256;  // unused
+        o.items_per_cta = h->items;
+    } else if (pick == SPMM_ALGO_MERGE) {
         // tasks per warp: AUTO takes tasks from a queue on skewed row lengths (R-MAT: the cost of equal
         // merge-path slices varies with their B rows' cache behaviour; measured -12% on R-MAT 22), and
         // one static task per warp otherwise (uniform costs: the queue's smaller tasks only add work)
@@ -523,7 +601,9 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             const long long workers = (long long)num_sms() * per_sm * tpw;
             const long long path = o.partition == SPMM_PARTITION_NONZERO_SPLIT ? h->nnz : h->m + h->nnz;
             long long it = (path + workers - 1) / workers;
-            it = std::max<long long>(256, (it + 31) / 32 * 32);
+            // queued tasks are kept >= MW_MIN_ITEMS_DYN items: smaller ones cost more in queue and carry
+            // traffic than they recover in balance (R-MAT 20, n = 1: 300-item tasks 24% slower)
+            it = std::max<long long>(tpw > 1 ? MW_MIN_ITEMS_DYN : 256, (it + 31) / 32 * 32);
             items = (int)std::min<long long>(it, 1LL << 30);
         }
         o.items_per_cta = items;
@@ -627,10 +707,11 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
     out->threshold = h->threshold;
     out->num_ctas = (int32_t)h->num_ctas;
     out->items_per_cta = h->chosen == SPMM_ALGO_MERGE ? h->items : 0;
-    out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : (h->rs_dyn ? 2 : 1));
-    out->compute_launch = (h->chosen == SPMM_ALGO_MERGE || h->rs_dyn) ? 1 : 0;
+    const bool rsq = h->chosen == SPMM_ALGO_ROWSPLIT && h->rs_dyn;
+    out->launches_per_execute = (h->m == 0) ? 0 : (h->chosen == SPMM_ALGO_MERGE ? 3 : (rsq ? 2 : 1));
+    out->compute_launch = (h->chosen == SPMM_ALGO_MERGE || rsq) ? 1 : 0;
     out->b_staging = (h->chosen == SPMM_ALGO_ROWSPLIT && h->capb > 0) ? 1 : 0;
-    out->rows_per_tile = h->chosen == SPMM_ALGO_ROWSPLIT ? h->rows_per_tile : 0;
+    out->rows_per_tile = (h->chosen == SPMM_ALGO_ROWSPLIT || h->chosen == SPMM_ALGO_TILED) ? h->rows_per_tile : 0;
     out->bspan_compact = h->bspan_compact;
     out->tasks_per_warp = h->chosen == SPMM_ALGO_MERGE ? h->opts.tasks_per_warp : 0;
     out->merge_worker_lanes = h->chosen == SPMM_ALGO_MERGE ? (h->mfold ? pick_fold(h->n, nullptr, h->n % 4 == 0 ? 4 : 1, nullptr, h->n % 4 == 0 ? 4 : 1).G : 32) : 0;

@@ -55,10 +55,11 @@ struct TileParams {
 // tile descriptor written by the producer next to the staged data
 struct TileInfo {
     int rs, zs, re, ze;  // rows [rs, re) of the tile, nonzeros [zs = ro[rs], ze = ro[re])
-    int ebase, zbase;    // global index of E[0] and of COL[0]/VAL[0]
+    int ebase, zbase;    // global index of E[0] and of COL[0]
     int range;           // row tile
     int flags;           // 1 first sub-tile, 2 last sub-tile, 4 staged, 8 done, 16 B span staged
     int blo;             // flags & 16: B row held at the start of the staged B span
+    int vbase;           // global index of VAL[0] (its own 16-byte phase: TMA copies align by address)
 };
 
 // one pipeline stage: row offsets | column indices | values | TileInfo (64 B) | B row span (capb bytes)
@@ -96,9 +97,6 @@ __device__ __forceinline__ int te_stage(void* dst, const void* src, long long be
     return (int)(a_al - mis);
 }
 
-// 16-byte granule phase of a 4-byte element array (TMA copies of two arrays share an index base only
-// when their phases agree)
-__device__ __forceinline__ int te_phase(const void* p) { return (int)((reinterpret_cast<uintptr_t>(p) >> 2) & 3); }
 
 // predicated vector gather of B (no branch): o valid only if pred
 template <int VEC> __device__ __forceinline__ void ldg_pred(unsigned (&o)[VEC], const void* p, bool pred);
@@ -253,6 +251,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             mbar_wait(&landed[pb], (ti / NS) & 1);
             TileInfo* ip = INFO_of(pb);
             const TileInfo pi = *ip;
+            __syncwarp();  // every lane has read the descriptor before lane 0 updates it below
             uint32_t btx = 0;
             const int cnt = pi.ze - pi.zs;
             if ((pi.flags & 4) && cnt > 0) {
@@ -286,7 +285,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
             if (lane == 0) mbar_arrive_expect_tx(&full[pb], btx);
         };
         const bool bstage = P.capb > 0;
-        const bool val_tma = te_phase(P.col) == te_phase(P.val);
         int pend = -1;  // B staging: tile index whose CSR slice is in flight
         // tiles: static round robin, or (merge; row split with irregular rows) taken from a global queue
         // so CTAs that finish early take more of the variable-cost tiles
@@ -311,7 +309,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 int b;
                 acquire(b);
                 uint64_t* csr_bar = bstage ? &landed[b] : &full[b];
-                uint32_t ptx_tx = 0;  // lane 0: TMA bytes of a tile whose values the warp copies
                 if (lane == 0) {
                     uint32_t tx = 0;
                     TileInfo inf;
@@ -323,29 +320,16 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                     inf.ebase = te_stage(E_of(b), P.ro, cr, nr + 1, (long long)m + 1, csr_bar, pol, &tx);
                     if (staged) {
                         inf.zbase = te_stage(COL_of(b), P.col, cz, nz, P.nnz, csr_bar, pol, &tx);
-                        // values share the column indices' index base when both arrays have the same
-                        // 16-byte phase (always for arrays sliced at the same offset); otherwise the
-                        // warp copies them below with plain loads
-                        if (val_tma) te_stage(VAL_of(b), P.val, cz, nz, P.nnz, csr_bar, pol, &tx);
+                        // the values get their own index base: the two arrays may sit at different
+                        // 16-byte phases (views at arbitrary offsets), and TMA copies align by address
+                        inf.vbase = te_stage(VAL_of(b), P.val, cz, nz, P.nnz, csr_bar, pol, &tx);
                     } else {
                         inf.zbase = 0;
+                        inf.vbase = 0;
                     }
                     inf.flags = (first ? 1 : 0) | (last ? 2 : 0) | (staged ? 4 : 0);
                     *INFO_of(b) = inf;
-                    if (val_tma || !staged) mbar_arrive_expect_tx(csr_bar, tx);
-                    else ptx_tx = tx;
-                }
-                if (!val_tma) {
-                    const TileInfo* ip = INFO_of(b);
-                    __syncwarp();
-                    if (ip->flags & 4) {
-                        const int zb = ip->zbase;
-                        for (long long p = cz + lane; p < nz; p += 32)
-                            static_cast<unsigned*>(static_cast<void*>(VAL_of(b)))[p - zb] =
-                                static_cast<const unsigned*>(P.val)[p];
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_expect_tx(csr_bar, ptx_tx);
-                    }
+                    mbar_arrive_expect_tx(csr_bar, tx);
                 }
                 __syncwarp();
                 if (bstage) {
@@ -464,13 +448,13 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                 const int maxlen = __reduce_max_sync(FULL, len);
                 if (staged) {
                     const uint32_t cs = smem_u32(COL) + 4u * (uint32_t)(s - inf.zbase);
-                    const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(s - inf.zbase);
+                    const uint32_t vs = smem_u32(VAL) + 4u * (uint32_t)(s - inf.vbase);
                     for (int p0 = 0; p0 < maxlen; p0 += U) {
                         const int rem = len - p0;
                         unsigned bv[U][NV][VEC];
                         unsigned cu[U], av[U];
                         const bool full_b = rem >= U;
-                        if (__all_sync(FULL, full_b && ((cs & 15u) == 0))) {  // full, 16B-aligned: LDS.128
+                        if (__all_sync(FULL, full_b && (((cs | vs) & 15u) == 0))) {  // full, 16B-aligned: LDS.128
 #pragma unroll
                             for (int u = 0; u < U; u += 4) {
                                 const uint4 c4 = lds_u128(cs + 4u * (p0 + u));

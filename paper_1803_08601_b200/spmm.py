@@ -25,7 +25,7 @@ SPMM_ERR_NOT_PLANNED = 4
 SPMM_ERR_WORKSPACE_TOO_SMALL = 5
 SPMM_ERR_UNSUPPORTED = 6
 SPMM_ERR_CUDA = 7
-SPMM_ALGO_AUTO, SPMM_ALGO_ROWSPLIT, SPMM_ALGO_MERGE = 0, 1, 2
+SPMM_ALGO_AUTO, SPMM_ALGO_ROWSPLIT, SPMM_ALGO_MERGE, SPMM_ALGO_TILED = 0, 1, 2, 3
 SPMM_F32, SPMM_I32 = 0, 1
 SPMM_PLUS_TIMES, SPMM_MIN_PLUS = 0, 1
 SPMM_FLAG_VALIDATE = 1
@@ -34,7 +34,7 @@ SPMM_PARTITION_MERGE_PATH, SPMM_PARTITION_NONZERO_SPLIT = 0, 1
 SPMM_MERGE_WORKER_AUTO, SPMM_MERGE_WORKER_WARP, SPMM_MERGE_WORKER_FOLDED = 0, 1, 2
 MERGE_WORKERS = {"auto": SPMM_MERGE_WORKER_AUTO, "warp": SPMM_MERGE_WORKER_WARP, "folded": SPMM_MERGE_WORKER_FOLDED}
 
-ALGOS = {"auto": SPMM_ALGO_AUTO, "rowsplit": SPMM_ALGO_ROWSPLIT, "merge": SPMM_ALGO_MERGE}
+ALGOS = {"auto": SPMM_ALGO_AUTO, "rowsplit": SPMM_ALGO_ROWSPLIT, "merge": SPMM_ALGO_MERGE, "tiled": SPMM_ALGO_TILED}
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 SEMIRINGS = {"plus_times": SPMM_PLUS_TIMES, "min_plus": SPMM_MIN_PLUS}
 

@@ -2,8 +2,8 @@
 """NEXT-4 measurement: the paper's Fig. 7 experiment on B200.
 
 A 100,000 x 100,000 matrix whose rows each hold a fixed percentage of nonzeros drawn without replacement
-(synth.uniform_rows, the paper's generator), times a 100,000 x 64 dense B, fp32.  Times the row-split and
-merge-based kernels (library-recorded CUDA events, L2 flushed before each rep) against a dense fp32 GEMM
+(synth.uniform_rows, the paper's generator), times a 100,000 x 64 dense B, fp32.  Times the row-split,
+merge-based and A/B-tiled (NEXT-4 second half) kernels (library-recorded CUDA events, L2 flushed before each rep) against a dense fp32 GEMM
 of the same product (torch.matmul -> cuBLAS sgemm, TF32 disabled: the fp32 CUDA-core GEMM, as the paper's
 cuBLAS sgemm), and reports the density at which the sparse path stops beating the dense one (the paper:
 merge-based SpMM beats GEMM below 9% fill on a K40c).  Sampled rows of each kernel are checked against the
@@ -82,7 +82,7 @@ def main():
         rows = np.unique(np.random.default_rng(d).integers(0, m, 64))
         pc = p.to("cpu")
         ref = oracle.spmm("f32_plus_times", m, k, n, pc.row_offsets, pc.col_indices, val.cpu(), B.cpu(), rows=rows)
-        for algo in ("rowsplit", "merge"):
+        for algo in ("rowsplit", "merge", "tiled"):
             op = S.CsrSpmm(p.row_offsets, p.col_indices, val, k)
             op.plan(n, algo)
             rec[f"{algo}_ms"] = time_spmm(op, B, C, flush, args.reps)
@@ -99,12 +99,13 @@ def main():
         rec["gemm_ms"] = time_gemm(A, B, flush, args.reps)
         del A
         torch.cuda.empty_cache()
-        best = min(rec["rowsplit_ms"], rec["merge_ms"])
+        best = min(rec["rowsplit_ms"], rec["merge_ms"], rec["tiled_ms"])
         rec["best_sparse_over_gemm"] = best / rec["gemm_ms"]
         res.append(rec)
         lines.append(f"{pct:6.2f}% d={d:6d} nnz={p.nnz:11d}  rowsplit {rec['rowsplit_ms']:9.3f} ms  merge "
-                     f"{rec['merge_ms']:9.3f} ms  sgemm {rec['gemm_ms']:9.3f} ms  best/gemm "
-                     f"{rec['best_sparse_over_gemm']:6.3f}  AUTO {rec['auto_pick']:8s}  parity {rec['rowsplit_parity'] and rec['merge_parity']}")
+                     f"{rec['merge_ms']:9.3f} ms  tiled {rec['tiled_ms']:9.3f} ms  sgemm {rec['gemm_ms']:9.3f} ms  "
+                     f"best/gemm {rec['best_sparse_over_gemm']:6.3f}  AUTO {rec['auto_pick']:8s}  parity "
+                     f"{rec['rowsplit_parity'] and rec['merge_parity'] and rec['tiled_parity']}")
         print(lines[-1], flush=True)
         del p, val
         torch.cuda.empty_cache()

@@ -752,3 +752,71 @@ def test_split_columns_kernel(pat):
             ins = (c >= c0) & (c < c1)
             assert np.array_equal(ci_[ri[r]:ri[r + 1]], c[ins] - c0) and np.array_equal(vi[ri[r]:ri[r + 1]], v[ins])
             assert np.array_equal(cx[rx[r]:rx[r + 1]], c[~ins]) and np.array_equal(vx[rx[r]:rx[r + 1]], v[~ins])
+
+
+# ------------------------------------------------------------------------------------------------
+# A/B-tiled kernel (NEXT-4): dense-ish rows, B streamed through shared memory in column blocks
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("n", [32, 36, 64, 96, 128])
+def test_tiled_parity(kind, n):
+    # rows of 0 / short / very long lengths (many B blocks per row, blocks with no entries)
+    lens = [0, 1, 7, 300, 2500, 0, 64] * 40 + [4000, 3]
+    p = synth.explicit_lengths(len(lens), 9000, lens, seed=9)
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    chosen, info = run_gpu(p, kind, n, "tiled", ro, ci, vd, Bd, Cd)
+    assert chosen == "tiled" and info["launches_per_execute"] == 1
+    check(p, kind, n, val, Bh, Cd)
+
+
+@pytest.mark.parametrize("kind", ["f32_plus_times", "i32_min_plus"])
+def test_tiled_padding_misalignment_and_epilogue(kind):
+    p = synth.uniform_rows(700, 3000, 400, 5)
+    for n, ldb, ldc, off in ((64, 70, 68, 0), (64, 64, 64, 1), (32, 33, 35, 3), (128, 128, 131, 2)):
+        val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, ldb=ldb, ldc=ldc, b_offset=off)
+        run_gpu(p, kind, n, "tiled", ro, ci, vd, Bd, Cd)
+        check(p, kind, n, val, Bh, Cd)
+    # accumulate + a peer copy
+    n = 64
+    val, Bh, ro, ci, vd, Bd, _ = make_inputs(p, kind, n)
+    C0 = synth.dense(p.m, n, 41, kind)
+    Cd = C0.to(DEV).clone()
+    peer = torch.zeros(p.m + 5, n, dtype=C0.dtype, device=DEV)
+    op = S.CsrSpmm(ro, ci, vd, p.k)
+    op.plan(n, "tiled", "plus_times" if kind.endswith("plus_times") else "min_plus")
+    op.execute(Bd, Cd, accumulate=True, peers=[peer.data_ptr()], peer_row_offset=5)
+    torch.cuda.synchronize()
+    op.close()
+    ref = oracle.spmm(kind, p.m, p.k, n, p.row_offsets, p.col_indices, val, Bh)
+    if kind == "f32_plus_times":
+        want = _combine_ref(kind, C0.numpy(), ref[0])
+        err = np.abs(Cd.cpu().numpy().astype(np.float64) - want)
+        assert (err <= 1e-5 * ref[1] + 2.0 ** -22 * np.abs(want) + 1e-30).all()
+    else:
+        assert np.array_equal(Cd.cpu().numpy(), _combine_ref(kind, C0.numpy(), ref))
+    assert torch.equal(peer[5:].cpu(), Cd.cpu())
+
+
+def test_tiled_bit_identical_and_preconditions():
+    p = synth.uniform_rows(900, 5000, 600, 8)
+    for kind in ("i32_plus_times", "f32_min_plus"):
+        outs = []
+        for algo in ("tiled", "merge", "rowsplit"):
+            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, 64)
+            run_gpu(p, kind, 64, algo, ro, ci, vd, Bd, Cd)
+            outs.append(Cd.cpu())
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    vd = synth.values(p.nnz, 1, "f32_plus_times").to(DEV)
+    op = S.CsrSpmm(p.row_offsets.to(DEV), p.col_indices.to(DEV), vd, p.k)
+    for bad_n in (30, 16, 132):
+        with pytest.raises(S.SpmmError) as e:
+            op.plan(bad_n, "tiled")
+        assert e.value.status == S.SPMM_ERR_UNSUPPORTED
+    op.close()
+    u = family("unsorted_duplicates")  # columns not sorted within rows: tiled must refuse
+    vu = synth.values(u.nnz, 1, "f32_plus_times").to(DEV)
+    op = S.CsrSpmm(u.row_offsets.to(DEV), u.col_indices.to(DEV), vu, u.k)
+    with pytest.raises(S.SpmmError) as e:
+        op.plan(64, "tiled")
+    assert e.value.status == S.SPMM_ERR_UNSUPPORTED
+    op.close()
