@@ -31,8 +31,17 @@
 #ifndef TL_MIN_D
 #define TL_MIN_D 1000000000.0  // AUTO picks the tiled kernel from this mean row length (set from the sweep)
 #endif
+#ifndef TL_TMA
+#define TL_TMA 1  // tiled: B blocks by TMA bulk copies (1) or cp.async from every thread (0)
+#endif
 #ifndef TL_RPG
 #define TL_RPG 4  // tiled: rows per row group (accumulators held across the whole K loop)
+#endif
+#ifndef RS_PAIRS
+#define RS_PAIRS 1  // row split, AUTO: consider the row-pair table for short rows
+#endif
+#ifndef RS_PAIR_MIN_SHARE
+#define RS_PAIR_MIN_SHARE 0.25  // row split, AUTO: use row pairs when this fraction of nonzeros is matched
 #endif
 #ifndef MW_MIN_ITEMS_DYN
 #define MW_MIN_ITEMS_DYN 1024  // merge, tasks from the queue: fewest items per task

@@ -10,8 +10,10 @@
 //              kb + 2 loads while block kb is consumed), the B tile of the dense-GEMM analogy.
 //   per block, every row advances a cursor over its (sorted) nonzeros: the entries with column < the
 //              block end are a prefix of what is left (no search, no format conversion -- the CSR is
-//              read once, 8 B per nonzero); a group loads G entries at a time (lane j: entry p + j),
-//              broadcasts them with shuffles and gathers the B rows from shared memory (LDS.128).
+//              read once, 8 B per nonzero); a group caches U entries of each of its rows in registers
+//              (lane j: entry p + j; the next batch is loaded while the current one is consumed), so a
+//              block a row has no entries in costs one ballot; entries are broadcast with shuffles and
+//              the B rows gathered from shared memory (LDS.128).
 // Requires column indices non-decreasing within each row (checked at plan time) and n % 4 == 0.
 #pragma once
 #include "common.cuh"
@@ -37,6 +39,7 @@ struct TiledParams {
     int kb;         // B rows per block
     int rows_per_cta;
     int b_vec4;     // B base 16-byte aligned and ldb % 4 == 0: 16-byte cp.async, else 4-byte
+    int b_tma;      // b_vec4: B blocks arrive by TMA bulk copies (one per block when ldb == n, else one per row)
     int c_vec4;     // C base 16-byte aligned and ldc % 4 == 0: float4 stores, else scalar
     EpiParams epi;
 };
@@ -46,11 +49,18 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+#ifndef TL_MINB
+#define TL_MINB 2  // CTAs per SM the register allocation targets
+#endif
+#ifndef TL_UMAX
+#define TL_UMAX 4  // entries per batch (B rows in flight per row group; 8 spills at 128 registers)
+#endif
+
 template <typename T, int SR, int G, int NV, int RPG>
-__global__ void __launch_bounds__(TL_THREADS, 2) k_tiled(const TiledParams P) {
+__global__ void __launch_bounds__(TL_THREADS, TL_MINB) k_tiled(const TiledParams P) {
     using R = Ring<T, SR>;
     constexpr int S = 32 / G;          // row groups per warp
-    constexpr int U = G < 8 ? G : 8;   // entries per batch (B rows in flight per group)
+    constexpr int U = G < TL_UMAX ? G : TL_UMAX;  // entries per batch (B rows in flight per group)
     extern __shared__ __align__(16) unsigned char tl_smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -81,6 +91,17 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_tiled(const TiledParams P) {
         p[i] = (r < P.m) ? __ldg(P.ro + r) : 0;
         e[i] = (r < P.m) ? __ldg(P.ro + r + 1) : 0;
     }
+    // the cached batch of each row: lane gl < U holds entry p + gl (INT_MAX past the row end)
+    int cc[RPG], off[RPG];
+    unsigned ca[RPG];
+#pragma unroll
+    for (int i = 0; i < RPG; ++i) {
+        const int idx = p[i] + gl;
+        const bool ok = gl < U && idx < e[i];
+        cc[i] = ok ? __ldg(P.col + idx) : 0x7fffffff;
+        ca[i] = ok ? __ldg(static_cast<const unsigned*>(P.val) + idx) : 0u;
+        off[i] = 0;
+    }
     T acc[RPG][NV][4];
 #pragma unroll
     for (int i = 0; i < RPG; ++i)
@@ -91,9 +112,40 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_tiled(const TiledParams P) {
 
     const int nblocks = (P.k + kb - 1) / kb;
     const int chunks_per_row = P.b_vec4 ? (n >> 2) : n;
-    // block b of B (rows [b kb, b kb + kb) ∩ [0, k)) into buffer (b & 1), all threads, one commit group
+    __shared__ __align__(8) uint64_t full[2];
+    if (P.b_tma) {
+        if (threadIdx.x == 0) {
+            mbar_init(&full[0], 1);
+            mbar_init(&full[1], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    const uint64_t pol = policy_evict_last();  // B blocks are re-read by every row tile: keep them in L2
+    // block b of B (rows [b kb, b kb + kb) ∩ [0, k)) into buffer (b & 1)
     auto load_block = [&](int b) {
-        if (b < nblocks) {
+        if (P.b_tma) {  // TMA: warp 0 issues, completion as transaction bytes on full[b & 1]
+            if (b < nblocks && warp == 0) {
+                const int k0 = b * kb;
+                const int rows = min(kb, P.k - k0);
+                const uint32_t rb = (uint32_t)n * 4u;
+                unsigned char* dst0 = tl_smem + (size_t)(b & 1) * buf_bytes;
+                const char* src0 = static_cast<const char*>(P.B) + (size_t)k0 * (size_t)P.ldb * 4u;
+                if (lane == 0) {
+                    fence_proxy_async_smem();
+                    mbar_arrive_expect_tx(&full[b & 1], (uint32_t)rows * rb);
+                }
+                __syncwarp();
+                if (P.ldb == n) {
+                    if (lane == 0) tma_load_1d(dst0, src0, (uint32_t)rows * rb, &full[b & 1], pol);
+                } else {
+                    for (int r = lane; r < rows; r += 32)
+                        tma_load_1d(dst0 + (size_t)r * rb, src0 + (size_t)r * (size_t)P.ldb * 4u, rb, &full[b & 1], pol);
+                }
+            }
+            return;
+        }
+        if (b < nblocks) {  // cp.async by every thread, one commit group per block
             const int k0 = b * kb;
             const int rows = min(kb, P.k - k0);
             const uint32_t dst0 = sbase + (uint32_t)(b & 1) * buf_bytes;
@@ -113,43 +165,61 @@ __global__ void __launch_bounds__(TL_THREADS, 2) k_tiled(const TiledParams P) {
     const int* __restrict__ colg = P.col;
     const unsigned* __restrict__ valg = static_cast<const unsigned*>(P.val);
     for (int b = 0; b < nblocks; ++b) {
-        cp_async_wait1();  // block b has landed (block b + 1 may still be in flight)
-        __syncthreads();
+        if (P.b_tma) {
+            mbar_wait(&full[b & 1], (uint32_t)((b >> 1) & 1));  // block b has landed
+        } else {
+            cp_async_wait1();  // block b has landed (block b + 1 may still be in flight)
+            __syncthreads();
+        }
         const int k0 = b * kb;
         const int khi = k0 + kb;
         const uint32_t bs = sbase + (uint32_t)(b & 1) * buf_bytes - (uint32_t)k0 * (uint32_t)npad * 4u;
 #pragma unroll
         for (int i = 0; i < RPG; ++i) {
             while (true) {
-                // the group's next U entries of row i (lane gl < U: entry p + gl)
-                const int idx = p[i] + gl;
-                const bool ok = gl < U && idx < e[i];
-                const int c = ok ? __ldg(colg + idx) : 0x7fffffff;
-                const unsigned a = ok ? __ldg(valg + idx) : 0u;
-                const unsigned inblk = __ballot_sync(FULL, c < khi);
-                // entries of this block are a prefix of the remaining ones (sorted columns)
+                // lanes [off, U) of the cached batch are row i's next unconsumed entries; those in this block
+                // are a prefix of them (sorted columns)
+                const bool mine = gl >= off[i] && gl < U;
+                const unsigned inblk = __ballot_sync(FULL, mine && cc[i] < khi);
                 const int cnt = __popc((inblk >> gbase) & ((1u << U) - 1u));
-                unsigned bv[U][NV][4];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int cu = __shfl_sync(FULL, c, gbase + u);
-#pragma unroll
-                    for (int v = 0; v < NV; ++v)
-                        lds_vpred<4>(bv[u][v], bs + ((uint32_t)cu * (uint32_t)npad + (uint32_t)cofs[v]) * 4u,
-                                     u < cnt && colok[v]);
+                const bool full = off[i] + cnt == U && p[i] + U < e[i];  // batch used up, the row goes on
+                int nc = 0x7fffffff;
+                unsigned na = 0u;
+                if (full) {  // next batch in flight while this one is consumed
+                    const int idx = p[i] + U + gl;
+                    if (gl < U && idx < e[i]) { nc = __ldg(colg + idx); na = __ldg(valg + idx); }
                 }
+                if (__any_sync(FULL, cnt > 0)) {
+                    unsigned bv[U][NV][4];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const T au = from_bits<T>(__shfl_sync(FULL, a, gbase + u));
-                    if (u < cnt) {
+                    for (int u = 0; u < U; ++u) {
+                        const int cu = __shfl_sync(FULL, cc[i], gbase + u);
+                        const bool take = u >= off[i] && u < off[i] + cnt;
 #pragma unroll
                         for (int v = 0; v < NV; ++v)
+                            lds_vpred<4>(bv[u][v], bs + ((uint32_t)cu * (uint32_t)npad + (uint32_t)cofs[v]) * 4u,
+                                         take && colok[v]);
+                    }
 #pragma unroll
-                            for (int x = 0; x < 4; ++x) acc[i][v][x] = R::mac(acc[i][v][x], au, from_bits<T>(bv[u][v][x]));
+                    for (int u = 0; u < U; ++u) {
+                        const T au = from_bits<T>(__shfl_sync(FULL, ca[i], gbase + u));
+                        if (u >= off[i] && u < off[i] + cnt) {
+#pragma unroll
+                            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) acc[i][v][x] = R::mac(acc[i][v][x], au, from_bits<T>(bv[u][v][x]));
+                        }
                     }
                 }
-                p[i] += cnt;
-                if (!__any_sync(FULL, cnt == U)) break;  // no group of the warp has more of this block
+                if (full) {
+                    p[i] += U;
+                    cc[i] = nc;
+                    ca[i] = na;
+                    off[i] = 0;
+                } else {
+                    off[i] += cnt;
+                }
+                if (!__any_sync(FULL, full)) break;  // no group of the warp has more of this block
             }
         }
         __syncthreads();  // every warp is done with buffer (b & 1)

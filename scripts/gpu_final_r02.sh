@@ -1,0 +1,33 @@
+#!/bin/bash
+# round 2 evidence on one B200: ncu traffic of the bench's kernels (profiles/ncu_traffic.json), launch lists,
+# ncu --set full summaries, the bench lines (default = configs[4], + heads 1 / 2, reference arm), the
+# config-3 n sweep, the scaling emulation of configs[4], full GPU suite + smoke.
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+O=gpurun_out/final
+mkdir -p $O
+NCU=/usr/local/cuda/bin/ncu
+timeout 3000 python scripts/ncu_traffic.py $O/ncu_traffic.json > $O/ncu_traffic.log 2>&1; echo "ncu_traffic rc=$?"
+cp $O/ncu_traffic.json profiles/ncu_traffic.json 2>/dev/null
+BARGS="--steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-extras"
+for c in 1 2 4; do
+  timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c$c.csv \
+    python bench.py --config $c $BARGS > /dev/null 2>&1; echo "launches c$c rc=$?"
+done
+for spec in "1 k_tile rowsplit_c1" "2 k_merge_w merge_c2"; do
+  set -- $spec
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$2 -s 2 -c 1 -f \
+    -o $O/prof_$3 python bench.py --config $1 $BARGS > /dev/null 2>&1
+  python scripts/ncu_summary.py $O/prof_$3.ncu-rep --stalls > $O/ncu_$3.txt 2>&1; echo "full $3 done"
+done
+timeout 1500 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo "bench default rc=$?"
+timeout 900 python bench.py --config 1 --no-extras > $O/bench_c1.json 2> $O/bench_c1.err; echo "bench c1 rc=$?"
+timeout 900 python bench.py --config 2 --no-extras > $O/bench_c2.json 2> $O/bench_c2.err; echo "bench c2 rc=$?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err; echo "bench ref rc=$?"
+cut -c1-400 $O/bench_default.json
+timeout 3000 python scripts/sweep_config4.py --out $O/config3 > $O/config3.log 2>&1; echo "config3 rc=$?"
+tail -8 $O/config3.log
+timeout 2400 python scripts/scaling_emulation.py --config 4 --out $O/scaling_emulation_config4 > $O/scaling4.log 2>&1; echo "scaling rc=$?"
+tail -7 $O/scaling4.log
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+tail -3 $O/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
