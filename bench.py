@@ -322,7 +322,7 @@ def measure_single(cfg: int, n: int, args, dev, flush_buf, sampler, peak, l2_byt
     t0 = time.perf_counter()
     op = S.CsrSpmm(p.row_offsets, p.col_indices, vals, p.k)
     chosen = op.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items,
-                     merge_worker=args.merge_worker, tasks_per_warp=args.tasks_per_warp, row_pairs=args.row_pairs)
+                     merge_worker=args.merge_worker, tasks_per_warp=args.tasks_per_warp)
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - t0) * 1e3
     info = op.info()
@@ -376,7 +376,6 @@ def main():
     ap.add_argument("--items", type=int, default=0)
     ap.add_argument("--merge-worker", default="auto", choices=["auto", "warp", "folded"])
     ap.add_argument("--tasks-per-warp", type=int, default=0)
-    ap.add_argument("--row-pairs", default="auto", choices=["auto", "off", "on"])
     ap.add_argument("--row-partition", type=int, default=1, help="multi-GPU: 0 nnz-balanced, 1 merge-path")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--gather-c", action="store_true", help="multi-GPU: also time the all-gather of C")
@@ -506,7 +505,7 @@ def measure_distributed(args, world, rank, dev, flush_buf, sampler, peak, sha, l
         vals = op.val
         del full, fvals
     chosen = op.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items,
-                     merge_worker=args.merge_worker, tasks_per_warp=args.tasks_per_warp, row_pairs=args.row_pairs)
+                     merge_worker=args.merge_worker, tasks_per_warp=args.tasks_per_warp)
     torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - t0) * 1e3
     info = op.info()
@@ -593,7 +592,7 @@ def run_e2e(args, ctx, n, world, rank, dev, sampler, flops_all, distributed):
             tdist.broadcast(B_d, src=0)
         o = S.CsrSpmm(ro_d, col_d, val_d, kg)
         o.plan(n, args.algo, "plus_times", partition=args.partition, items_per_cta=args.items,
-                     merge_worker=args.merge_worker, tasks_per_warp=args.tasks_per_warp, row_pairs=args.row_pairs)
+                     merge_worker=args.merge_worker, tasks_per_warp=args.tasks_per_warp)
         o.execute(B_d, C_d)
         C_h.copy_(C_d, non_blocking=True)
         o.close()

@@ -46,8 +46,7 @@ extern "C" {
  * need a 256-byte workspace (tile queue) -- callers must size the workspace from plan(); 4 = plan
  * option merge_worker (was reserved0), plan option tasks_per_warp (was reserved[0]) and
  * spmm_plan_info.merge_worker_lanes / tasks_per_warp (lane-folded merge, task queue),
- * spmm_csr_execute_ex (accumulate, peer copies of C) and the spmm_ipc_* buffers, SPMM_ALGO_TILED, plan
- * option row_pairs (was reserved[1]) with spmm_plan_info.row_pairs / pair_share. */
+ * spmm_csr_execute_ex (accumulate, peer copies of C) and the spmm_ipc_* buffers, SPMM_ALGO_TILED. */
 #define SPMM_ABI_VERSION 4
 
 typedef struct spmm_csr_s* spmm_csr_t;
@@ -73,7 +72,6 @@ enum { SPMM_FLAG_VALIDATE = 1u };                                       /* one c
 typedef enum { SPMM_POLICY_AUTO = 0, SPMM_POLICY_PAPER = 1 } spmm_policy;
 typedef enum { SPMM_PARTITION_MERGE_PATH = 0, SPMM_PARTITION_NONZERO_SPLIT = 1 } spmm_partition;
 typedef enum { SPMM_MERGE_WORKER_AUTO = 0, SPMM_MERGE_WORKER_WARP = 1, SPMM_MERGE_WORKER_FOLDED = 2 } spmm_merge_worker;
-typedef enum { SPMM_ROW_PAIRS_AUTO = 0, SPMM_ROW_PAIRS_OFF = 1, SPMM_ROW_PAIRS_ON = 2 } spmm_row_pairs;
 
 /* Optional planner knobs (spmm_csr_plan_ex).  Zero-initialised = defaults. */
 typedef struct {
@@ -100,12 +98,7 @@ typedef struct {
                                 1 = one task per warp, walked in a static order; k > 1 = k tasks per
                                 warp taken from a queue in the workspace (zeroed by the partition
                                 kernel) so warps that finish early take more.  At most 64.          */
-    int32_t row_pairs;       /* spmm_row_pairs, row split only.  AUTO (0): for short rows (d <= 32, rows of
-                                >= 64 bytes of B) plan builds a row-pair table (one pass over the CSR,
-                                8 bytes per pair, owned by the handle) and uses it when >= 25% of the
-                                nonzeros of row 2i+1 share a column with row 2i at a common shift, so
-                                one B-row read feeds both rows.  OFF (1) / ON (2) force it.        */
-    int32_t reserved[2];     /* must be zero */
+    int32_t reserved[3];     /* must be zero */
 } spmm_plan_opts;
 
 /* Read-only description of the current plan (spmm_csr_get_plan_info). */
@@ -131,8 +124,6 @@ typedef struct {
     int32_t merge_worker_lanes; /* merge: lanes per merge worker (32 = whole warp, G < 32 = lane-folded
                                    slots, with 16-byte aligned B / C); 0 for row split              */
     int32_t tasks_per_warp;  /* merge: tasks per resident warp the plan sized (> 1: taken from a queue) */
-    int32_t row_pairs;       /* row split: 1 if the row-pair table is used                              */
-    double pair_share;       /* matched nonzeros / nnz of the row-pair table (-1: not built)            */
 } spmm_plan_info;
 
 /*

@@ -37,12 +37,6 @@
 #ifndef TL_RPG
 #define TL_RPG 4  // tiled: rows per row group (accumulators held across the whole K loop)
 #endif
-#ifndef RS_PAIRS
-#define RS_PAIRS 1  // row split, AUTO: consider the row-pair table for short rows
-#endif
-#ifndef RS_PAIR_MIN_SHARE
-#define RS_PAIR_MIN_SHARE 0.25  // row split, AUTO: use row pairs when this fraction of nonzeros is matched
-#endif
 #ifndef MW_MIN_ITEMS_DYN
 #define MW_MIN_ITEMS_DYN 1024  // merge, tasks from the queue: fewest items per task
 #endif

@@ -42,9 +42,6 @@ struct spmm_csr_s {
     double bspan_compact = -1.0;  // fraction of nonzeros in row tiles whose B span is compact (plan-time)
     int32_t tl_kb = 0;            // tiled: B rows per shared-memory block
     int sorted = -1;              // column indices non-decreasing within rows: -1 unknown, 0 no, 1 yes
-    uint2* d_pairs = nullptr;     // row split: row-pair table (handle-owned, 8 bytes per pair), or null
-    bool rs_pairs = false;        // row split: the plan uses the row-pair table
-    double pair_share = -1.0;     // matched entries / nnz of the row-pair table (-1: not measured)
     size_t ws_bytes = 0;
     int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
@@ -158,42 +155,6 @@ __global__ void k_check_sorted(const int* __restrict__ ro, const int* __restrict
         for (int q = s + 1 + lane; q < e; q += 32) bad |= (col[q] < col[q - 1]) ? 1 : 0;
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(flag, 1);
-}
-
-// row-pair table (row split): thread per pair (2i, 2i+1) of rows with at most 32 entries each.
-// delta = position in the first row of the second row's first column (0 if absent); bit j of the mask
-// = entry j of the first row has the column of entry j - delta of the second row.  y = delta | 256 when
-// the pair shares at least one column (paired), else 0.  out_cnt += matched entries.
-__global__ void k_pair_info(const int* __restrict__ ro, const int* __restrict__ col, long long m,
-                            uint2* __restrict__ info, unsigned long long* __restrict__ out_cnt) {
-    unsigned long long tot = 0;
-    const long long npairs = (m + 1) / 2;
-    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < npairs;
-         q += (long long)gridDim.x * blockDim.x) {
-        const long long a = 2 * q;
-        uint2 r = make_uint2(0u, 0u);
-        if (a + 1 < m) {
-            const int sA = ro[a], sB = ro[a + 1], eB = ro[a + 2];
-            const int lenA = sB - sA, lenB = eB - sB;
-            if (lenA > 0 && lenB > 0 && lenA <= 32 && lenB <= 32) {
-                const int b0 = col[sB];
-                int dl = -1;
-                for (int j = 0; j < lenA; ++j)
-                    if (col[sA + j] == b0) { dl = j; break; }
-                unsigned mask = 0u;
-                if (dl >= 0)
-                    for (int j = dl; j < lenA && j - dl < lenB; ++j)
-                        if (col[sA + j] == col[sB + j - dl]) mask |= 1u << j;
-                if (mask) {
-                    r = make_uint2(mask, (unsigned)dl | 256u);
-                    tot += (unsigned long long)__popc(mask);
-                }
-            }
-        }
-        info[q] = r;
-    }
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(FULL, tot, o);
-    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(out_cnt, tot);
 }
 
 // flags: bit0 ro[0] != 0, bit1 decreasing offsets, bit2 ro[m] != nnz, bit3 column out of range
@@ -397,7 +358,6 @@ cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, lo
     }
     if (h->chosen == SPMM_ALGO_ROWSPLIT) {
         P.tile_ctr = static_cast<int*>(ws);
-        P.pair_info = h->rs_pairs ? h->d_pairs : nullptr;
         return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), P, st);
     }
     const VecCfg mc = h->mfold ? pick_fold(h->n, Bv, ldb, Cv, ldc) : pick_vec(h->n, Bv, ldb, Cv, ldc, false);
@@ -420,29 +380,6 @@ static spmm_status measure_max_row(spmm_csr_t h, void* stream) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(h, e, "plan: max row length");
     h->max_row = hmax;
-    return SPMM_OK;
-}
-
-// plan-time row-pair table (row split): one pass over the CSR, handle-owned buffer (A is immutable while
-// the handle lives, so the table is built once)
-static spmm_status build_pairs(spmm_csr_t h, void* stream) {
-    if (h->d_pairs) return SPMM_OK;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const long long npairs = (h->m + 1) / 2;
-    cudaError_t e = cudaMalloc(&h->d_pairs, sizeof(uint2) * (size_t)std::max<long long>(npairs, 1));
-    if (e != cudaSuccess) { h->d_pairs = nullptr; return cuda_fail(h, e, "plan: row-pair table"); }
-    unsigned long long cnt = 0;
-    unsigned long long* dc = reinterpret_cast<unsigned long long*>(h->d_scratch + 4);
-    e = cudaMemsetAsync(dc, 0, sizeof(cnt), st);
-    if (e == cudaSuccess) {
-        const int grid = (int)std::min<long long>((npairs + THREADS - 1) / THREADS, 16LL * kNumSMs);
-        k_pair_info<<<std::max(grid, 1), THREADS, 0, st>>>(h->ro, h->col, h->m, h->d_pairs, dc);
-        e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&cnt, dc, sizeof(cnt), cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(h, e, "plan: row-pair table");
-    h->pair_share = h->nnz > 0 ? (double)cnt / (double)h->nnz : 0.0;
     return SPMM_OK;
 }
 
@@ -538,7 +475,6 @@ spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, 
 
 spmm_status spmm_csr_destroy(spmm_csr_t h) {
     if (!h) return SPMM_OK;
-    if (h->d_pairs) cudaFree(h->d_pairs);
     if (h->d_scratch) cudaFree(h->d_scratch);
     delete h;
     return SPMM_OK;
@@ -562,7 +498,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     if (sr != SPMM_PLUS_TIMES && sr != SPMM_MIN_PLUS) return fail(h, SPMM_ERR_INVALID_ARG, "bad semiring");
     spmm_plan_opts o{};
     if (opts) o = *opts;
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 3; ++i)
         if (o.reserved[i] != 0) return fail(h, SPMM_ERR_INVALID_ARG, "reserved plan option fields must be 0");
     if (o.merge_worker < 0 || o.merge_worker > 2) return fail(h, SPMM_ERR_INVALID_ARG, "bad merge_worker");
     if (o.tasks_per_warp < 0 || o.tasks_per_warp > 64) return fail(h, SPMM_ERR_INVALID_ARG, "tasks_per_warp must be in [0, 64]");
@@ -586,8 +522,6 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     h->capb = 0;
     h->bspan_compact = -1.0;
     h->rs_dyn = false;
-    h->rs_pairs = false;
-    if (o.row_pairs < 0 || o.row_pairs > 2) return fail(h, SPMM_ERR_INVALID_ARG, "bad row_pairs");
     const double d = h->m > 0 ? (double)h->nnz / (double)h->m : 0.0;  // PAPER.md:267, mean row length
     spmm_algo pick = algo;
     if (algo == SPMM_ALGO_AUTO) {
@@ -739,14 +673,6 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
         }
         R = h->rows_per_tile;
         h->num_ctas = (h->m + R - 1) / R;
-        // row pairs (one B row read feeds two rows where adjacent rows share columns): a plan-time table,
-        // used when at least RS_PAIR_MIN_SHARE of the nonzeros are matched (AUTO), or forced
-        if (o.row_pairs == SPMM_ROW_PAIRS_ON ||
-            (o.row_pairs == SPMM_ROW_PAIRS_AUTO && RS_PAIRS && h->m > 1 && d <= 32.0 && (size_t)n * elem >= 64)) {
-            const spmm_status ps = build_pairs(h, stream);
-            if (ps != SPMM_OK) return ps;
-            h->rs_pairs = o.row_pairs == SPMM_ROW_PAIRS_ON || h->pair_share >= RS_PAIR_MIN_SHARE;
-        }
         // irregular (but not merge-skewed) row lengths: uneven tile costs, so the persistent CTAs take
         // row tiles from a queue (measured: lognormal d = 7.9 -14%; regular matrices keep the static
         // round robin, which the queue's extra latency slows)
@@ -789,8 +715,6 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
     out->rows_per_tile = (h->chosen == SPMM_ALGO_ROWSPLIT || h->chosen == SPMM_ALGO_TILED) ? h->rows_per_tile : 0;
     out->bspan_compact = h->bspan_compact;
     out->tasks_per_warp = h->chosen == SPMM_ALGO_MERGE ? h->opts.tasks_per_warp : 0;
-    out->row_pairs = (h->chosen == SPMM_ALGO_ROWSPLIT && h->rs_pairs) ? 1 : 0;
-    out->pair_share = h->pair_share;
     out->merge_worker_lanes = h->chosen == SPMM_ALGO_MERGE ? (h->mfold ? pick_fold(h->n, nullptr, h->n % 4 == 0 ? 4 : 1, nullptr, h->n % 4 == 0 ? 4 : 1).G : 32) : 0;
     out->workspace_bytes = h->ws_bytes;
     return SPMM_OK;

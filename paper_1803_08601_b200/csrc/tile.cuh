@@ -49,7 +49,6 @@ struct TileParams {
     int stages;         // shared-memory pipeline depth (2..TE_MAX_STAGES)
     int capb;           // rowsplit: bytes per stage for the tile's B row span (0 = B is gathered from global)
     int* tile_ctr;      // tile queue (irregular rows; zeroed before the launch); null = static round robin
-    const uint2* pair_info;  // row pairs (plan-time table, one entry per pair (2i, 2i+1)); null = unpaired
     EpiParams epi;      // accumulate / peer copies of finished rows
 };
 
@@ -512,82 +511,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
                     }
                 }
             };
-            // Row pairs (plan-time table: the B access pattern has the greatest impact):
-            // a group owns rows (2i, 2i+1); entry j of the first row and entry j - delta of the second share
-            // a column when bit j of the pair's mask is set, so ONE B row read into registers feeds both
-            // rows; the second row's unmatched entries follow.  Every stored entry is used exactly once.
-            auto pair_pass = [&](const bool kS, const int sA, const int lenA, const int sB, const int lenB,
-                                 const unsigned mA, const int dl, Acc<T, SR, VEC, NV>& accA,
-                                 Acc<T, SR, VEC, NV>& accB) {
-                const uint32_t csA = smem_u32(COL) + 4u * (uint32_t)(sA - inf.zbase);
-                const uint32_t vsA = smem_u32(VAL) + 4u * (uint32_t)(sA - inf.vbase);
-                const uint32_t csB = smem_u32(COL) + 4u * (uint32_t)(sB - inf.zbase);
-                const uint32_t vsB = smem_u32(VAL) + 4u * (uint32_t)(sB - inf.vbase);
-                const uint32_t vsBd = vsB - 4u * (uint32_t)dl;  // value of the second row's entry j - delta
-                const int maxA = __reduce_max_sync(FULL, lenA);
-                for (int p0 = 0; p0 < maxA; p0 += U) {
-                    const int rem = lenA - p0;
-                    unsigned bv[U][NV][VEC];
-                    unsigned cu[U], av[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        cu[u] = lds_pred(csA + 4u * (p0 + u), u < rem);
-                        av[u] = lds_pred(vsA + 4u * (p0 + u), u < rem);
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], u < rem);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        if (u < rem) accA.mac(from_bits<T>(av[u]), bv[u]);
-                        const int j = p0 + u;
-                        const bool mt = u < rem && j < 32 && ((mA >> (j & 31)) & 1u);
-                        const unsigned bvl = lds_pred(vsBd + 4u * (uint32_t)j, mt);
-                        if (mt) accB.mac(from_bits<T>(bvl), bv[u]);
-                    }
-                }
-                const unsigned mB = mA >> dl;
-                const int maxB = __reduce_max_sync(FULL, lenB);
-                for (int p0 = 0; p0 < maxB; p0 += U) {
-                    bool need[U];
-                    unsigned bv[U][NV][VEC];
-                    unsigned cu[U], av[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int i = p0 + u;
-                        need[u] = i < lenB && !(i < 32 && ((mB >> (i & 31)) & 1u));
-                        cu[u] = lds_pred(csB + 4u * (uint32_t)i, need[u]);
-                        av[u] = lds_pred(vsB + 4u * (uint32_t)i, need[u]);
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) GP(kS, bv[u], (int)cu[u], need[u]);
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (need[u]) accB.mac(from_bits<T>(av[u]), bv[u]);
-                }
-            };
-            if (P.pair_info && staged) {
-                const int npairs = (rows + 1) >> 1;
-                const int rounds = (npairs + NG - 1) / NG;
-                for (int t = 0; t < rounds; ++t) {
-                    const int lp = t * NG + gid;
-                    const bool active = lp < npairs;
-                    const int rA = inf.rs + 2 * lp;
-                    const bool hasB = active && 2 * lp + 1 < rows;
-                    const int sA = active ? E[rA - inf.ebase] : 0;
-                    const int eA = active ? E[rA + 1 - inf.ebase] : 0;
-                    const int eB = hasB ? E[rA + 2 - inf.ebase] : eA;
-                    const uint2 pi = active ? __ldg(P.pair_info + (rA >> 1)) : make_uint2(0u, 0u);
-                    const unsigned mA = (pi.y & 256u) ? pi.x : 0u;
-                    const int dl = (pi.y & 256u) ? (int)(pi.y & 255u) : 0;
-                    Acc<T, SR, VEC, NV> accA, accB;
-                    accA.reset();
-                    accB.reset();
-                    if (bsm) pair_pass(true, sA, eA - sA, eA, eB - eA, mA, dl, accA, accB);
-                    else pair_pass(false, sA, eA - sA, eA, eB - eA, mA, dl, accA, accB);
-                    store_row(rA, accA, active);
-                    store_row(rA + 1, accB, hasB);
-                }
-            } else {
+            {
                 const int rounds = (rows + NG - 1) / NG;
                 for (int t = 0; t < rounds; ++t) {
                     const int lr = t * NG + gid;

@@ -49,8 +49,7 @@ SPMM_IPC_HANDLE_BYTES = 64
 
 class spmm_plan_opts(Structure):
     _fields_ = [("policy", c_int32), ("partition", c_int32), ("items_per_cta", c_int32),
-                ("merge_worker", c_int32), ("tasks_per_warp", c_int32), ("row_pairs", c_int32),
-                ("reserved", c_int32 * 2)]
+                ("merge_worker", c_int32), ("tasks_per_warp", c_int32), ("reserved", c_int32 * 3)]
 
 
 class spmm_plan_info(Structure):
@@ -60,7 +59,7 @@ class spmm_plan_info(Structure):
                 ("num_ctas", c_int32), ("items_per_cta", c_int32), ("launches_per_execute", c_int32),
                 ("compute_launch", c_int32), ("workspace_bytes", c_size_t), ("b_staging", c_int32),
                 ("rows_per_tile", c_int32), ("bspan_compact", c_double), ("merge_worker_lanes", c_int32),
-                ("tasks_per_warp", c_int32), ("row_pairs", c_int32), ("pair_share", c_double)]
+                ("tasks_per_warp", c_int32)]
 
 
 class spmm_exec_opts(Structure):
@@ -160,8 +159,8 @@ def spmm_csr_plan(h, n, algo, semiring, threshold=0.0, stream=None):
 
 
 def spmm_csr_plan_ex(h, n, algo, semiring, threshold=0.0, policy=0, partition=0, items_per_cta=0, stream=None,
-                     merge_worker=0, tasks_per_warp=0, row_pairs=0):
-    o = spmm_plan_opts(policy, partition, items_per_cta, merge_worker, tasks_per_warp, row_pairs)
+                     merge_worker=0, tasks_per_warp=0):
+    o = spmm_plan_opts(policy, partition, items_per_cta, merge_worker, tasks_per_warp)
     ws = c_size_t(0)
     chosen = c_int32(0)
     st = load().spmm_csr_plan_ex(h, n, algo, semiring, threshold, ctypes.byref(o), stream, ctypes.byref(ws),
@@ -288,14 +287,13 @@ class CsrSpmm:
 
     def plan(self, n: int, algo: str = "auto", semiring: str = "plus_times", threshold: float = 0.0,
              policy: str = "auto", partition: str = "merge_path", items_per_cta: int = 0, stream=None,
-             merge_worker: str = "auto", tasks_per_warp: int = 0, row_pairs: str = "auto") -> str:
+             merge_worker: str = "auto", tasks_per_warp: int = 0) -> str:
         import torch
         st, ws, chosen = spmm_csr_plan_ex(self._h, n, ALGOS[algo], SEMIRINGS[semiring], threshold,
                                           {"auto": SPMM_POLICY_AUTO, "paper": SPMM_POLICY_PAPER}[policy],
                                           {"merge_path": SPMM_PARTITION_MERGE_PATH,
                                            "nonzero_split": SPMM_PARTITION_NONZERO_SPLIT}[partition],
-                                          items_per_cta, _stream_ptr(stream), MERGE_WORKERS[merge_worker], tasks_per_warp,
-                                          {"auto": 0, "off": 1, "on": 2}[row_pairs])
+                                          items_per_cta, _stream_ptr(stream), MERGE_WORKERS[merge_worker], tasks_per_warp)
         _check(st, self._h)
         self.n = n
         self.workspace = torch.empty(max(ws, 16), dtype=torch.uint8, device=self.row_offsets.device)

@@ -820,52 +820,3 @@ def test_tiled_bit_identical_and_preconditions():
         op.plan(64, "tiled")
     assert e.value.status == S.SPMM_ERR_UNSUPPORTED
     op.close()
-
-
-# ------------------------------------------------------------------------------------------------
-# row split with the plan-time row-pair table (one B-row read feeds rows 2i and 2i+1)
-# ------------------------------------------------------------------------------------------------
-def _pair_patterns():
-    return {"banded": synth.banded(3001, lo=5, hi=9), "banded16": synth.banded(4099),
-            "uniform": synth.uniform_rows(1500, 1200, 9, 21), "lengths_1_31_32_33": family("lengths_1_31_32_33"),
-            "unsorted_duplicates": family("unsorted_duplicates"), "many_empty_rows": family("many_empty_rows"),
-            "leading_trailing_empty": family("leading_trailing_empty")}
-
-
-_PP = {}
-
-
-@pytest.mark.parametrize("pat", ["banded", "banded16", "uniform", "lengths_1_31_32_33", "unsorted_duplicates",
-                                 "many_empty_rows", "leading_trailing_empty"])
-@pytest.mark.parametrize("kind", synth.KINDS)
-@pytest.mark.parametrize("n", [16, 33, 64, 128])
-def test_row_pairs_parity(pat, kind, n):
-    if not _PP:
-        _PP.update(_pair_patterns())
-    p = _PP[pat]
-    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
-    _, info = run_gpu(p, kind, n, "rowsplit", ro, ci, vd, Bd, Cd, row_pairs="on")
-    assert info["row_pairs"] == 1
-    check(p, kind, n, val, Bh, Cd)
-
-
-def test_row_pairs_bit_identical_and_auto():
-    p = synth.banded(5001)
-    for kind in ("i32_plus_times", "i32_min_plus", "f32_min_plus"):
-        outs = []
-        for rp in ("off", "on"):
-            val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, 64)
-            _, info = run_gpu(p, kind, 64, "rowsplit", ro, ci, vd, Bd, Cd, row_pairs=rp)
-            assert info["row_pairs"] == (1 if rp == "on" else 0)
-            outs.append(Cd.cpu())
-        assert torch.equal(outs[0], outs[1])
-    # AUTO: banded rows share 15 of 16 columns with their neighbour -> pairs; uniform random rows do not
-    for pat, want in ((synth.banded(1 << 14), 1), (synth.uniform_rows(1 << 14, 1 << 14, 16, 3), 0)):
-        vd = synth.values(pat.nnz, 1, "f32_plus_times").to(DEV)
-        op = S.CsrSpmm(pat.row_offsets.to(DEV), pat.col_indices.to(DEV), vd, pat.k)
-        assert op.plan(64, "auto") == "rowsplit"
-        inf = op.info()
-        assert inf["row_pairs"] == want, inf
-        if want:
-            assert inf["pair_share"] > 0.9
-        op.close()
