@@ -547,7 +547,13 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             // would stream A from global per row group (measured 2.5x slower than merge at d = 1000,
             // profiles/r01_density_sweep.txt), while merge path stages fixed-size slices at any d
             const bool long_rows = RS_ZF / 10.0 * 16.0 * d > (double)(RS_CAPZ_MAX - 8);
-            pick = (skewed || few_rows || long_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
+            // (round 2 refit on the config-3 sweep, profiles/r02_config3_summary.txt, with the task queue
+            // and the lane-folded workers): merge path also wins for mildly skewed rows (max row above 16 d
+            // but under the 1024 floor) once B rows are >= 64 bytes, and for very short rows with wide B
+            // (the row-split tiles then carry 1-4 nonzeros per row of per-row overhead)
+            const bool mild_skew = (double)hmax > 16.0 * d && hmax >= 256 && n >= 16;
+            const bool short_rows = (d < 3.0 && n >= 32) || (d <= 4.0 && n > 64);
+            pick = (skewed || few_rows || long_rows || mild_skew || short_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
             // dense-ish rows (NEXT-4): B streamed once per row tile beats a B-row gather
             // per nonzero once d is large (measured crossover)
             if (d >= TL_MIN_D && !skewed && tiled_shape_ok(n)) {

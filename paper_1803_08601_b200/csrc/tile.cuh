@@ -1,5 +1,5 @@
 // tile.cuh -- Algorithm I, row-splitting SpMM (§4.1), as a persistent,
-// warp-specialised "tile engine" for sm_100a.  (Algorithm II, merge-based, is merge_w.cuh.)
+// warp-specialised "tile engine" for sm_100a.  (Algorithm II, merge-based, is merge_w.cuh / merge_f.cuh.)
 //
 //   warp 8 (producer, one elected lane issues): walks this CTA's tiles, computes each tile's bounds
 //     and stages the tile's slice of A -- row offsets, column indices, values -- into shared memory
@@ -286,7 +286,7 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
         };
         const bool bstage = P.capb > 0;
         int pend = -1;  // B staging: tile index whose CSR slice is in flight
-        // tiles: static round robin, or (merge; row split with irregular rows) taken from a global queue
+        // tiles: static round robin, or (irregular rows) taken from a global queue
         // so CTAs that finish early take more of the variable-cost tiles
         auto next_tile = [&](int cur) -> int {
             if (P.tile_ctr) {
@@ -359,9 +359,6 @@ __device__ __forceinline__ void tile_body(const TileParams& P) {
 
     // =============================== consumer warps ===============================
     constexpr int S = 32 / G;
-#ifndef MG_NA
-#define MG_NA 1  // merge: accumulator sets per worker (1 measured 1-10% faster than 2 or 4)
-#endif
 #ifndef RS_NA
 #define RS_NA 1  // row split: one accumulator set per row (measured 1-7% faster than 2 interleaved)
 #endif

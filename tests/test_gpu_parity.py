@@ -281,13 +281,13 @@ def test_auto_few_rows_guard_needs_enough_work():
 @pytest.mark.parametrize("kind", synth.KINDS)
 @pytest.mark.parametrize("n", [8, 64, 128])
 def test_rowsplit_tile_queue_for_irregular_rows(kind, n):
-    # lognormal rows (max row >> mean, but below the merge skew guard): AUTO keeps row split and takes
-    # the row tiles from a queue in the workspace (256 bytes); results unchanged
+    # lognormal rows (max row >> mean): row split under the AUTO policy takes the row tiles from a
+    # queue in the workspace (256 bytes); results unchanged
     p = synth.lognormal_rows(20000, 9000, 7.92, 77)
     val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
     sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
     op = S.CsrSpmm(ro, ci, vd, p.k)
-    assert op.plan(n, "auto", sr) == "rowsplit"
+    assert op.plan(n, "rowsplit", sr) == "rowsplit"
     info = op.info()
     assert info["workspace_bytes"] == 256 and info["launches_per_execute"] == 2 and info["compute_launch"] == 1
     op.execute(Bd, Cd)
@@ -300,6 +300,24 @@ def test_rowsplit_tile_queue_for_irregular_rows(kind, n):
     torch.cuda.synchronize()
     op.close()
     check(p, kind, n, val, Bh, Cd)
+
+
+def test_auto_refit_guards():
+    """Round-2 refit of AUTO (profiles/r02_config3_summary.txt): mildly skewed rows with n >= 16 and very
+    short rows with wide B go to merge; banded short rows and narrow B stay on row split."""
+    cases = ((synth.lognormal_rows(1 << 16, 1 << 16, 7.92, 87), 64, "merge"),
+             (synth.lognormal_rows(1 << 16, 1 << 16, 7.92, 87), 4, "rowsplit"),
+             (synth.uniform_rows(1 << 16, 1 << 16, 1, 5), 64, "merge"),
+             (synth.uniform_rows(1 << 16, 1 << 16, 1, 5), 16, "rowsplit"),
+             (synth.uniform_rows(1 << 16, 1 << 16, 4, 5), 128, "merge"),
+             (synth.banded(1 << 16, 2, 2), 64, "rowsplit"))
+    for pat, n, want in cases:
+        vd = synth.values(pat.nnz, 1, "f32_plus_times").to(DEV)
+        op = S.CsrSpmm(pat.row_offsets.to(DEV), pat.col_indices.to(DEV), vd, pat.k)
+        got = op.plan(n, "auto")
+        inf = op.info()
+        op.close()
+        assert got == want, (pat.name, n, inf["mean_row_length"], inf["max_row_length"])
 
 
 def test_auto_picks_merge_for_rows_too_long_to_stage():
