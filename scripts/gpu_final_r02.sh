@@ -10,12 +10,13 @@ timeout 3000 python scripts/ncu_traffic.py $O/ncu_traffic.json > $O/ncu_traffic.
 cp $O/ncu_traffic.json profiles/ncu_traffic.json 2>/dev/null
 BARGS="--steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-extras"
 for c in 1 2 4; do
-  timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c$c.csv \
+  timeout 1500 $NCU --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k "regex:k_tile|k_merge_|k_partition|k_fixup|k_max_row|k_tiled" \
+    --csv --log-file $O/launches_c$c.csv \
     python bench.py --config $c $BARGS > /dev/null 2>&1; echo "launches c$c rc=$?"
 done
-for spec in "1 k_tile rowsplit_c1" "2 k_merge_w merge_c2"; do
+for spec in "1 k_tile< rowsplit_c1" "2 k_merge_w< merge_c2"; do
   set -- $spec
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$2 -s 2 -c 1 -f \
+  timeout 900 $NCU --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$2" -s 2 -c 1 -f \
     -o $O/prof_$3 python bench.py --config $1 $BARGS > /dev/null 2>&1
   python scripts/ncu_summary.py $O/prof_$3.ncu-rep --stalls > $O/ncu_$3.txt 2>&1; echo "full $3 done"
 done

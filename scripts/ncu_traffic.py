@@ -16,7 +16,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NCU = "/usr/local/cuda/bin/ncu"
 METRICS = "dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,gpu__time_duration.sum"
-KERNEL = {"rowsplit": ("regex:k_tile", "k_tile<ROWSPLIT>"), "merge": ("regex:k_merge_[wf]", "k_merge_w")}
+# demangled-name filters: the compute kernels only (not the plan-time k_tile_span etc.)
+KERNEL = {"rowsplit": ("regex:k_tile<", "k_tile<ROWSPLIT>"), "merge": ("regex:k_merge_[wf]<", "k_merge_w")}
 
 
 def sha16():
@@ -26,7 +27,8 @@ def sha16():
 
 def capture(cfg, algo_kind, full):
     kregex, kname = KERNEL[algo_kind]
-    cmd = [NCU, "--clock-control", "none", "-k", kregex, "-s", "1", "-c", "1", "--csv", "--page", "raw"]
+    cmd = [NCU, "--clock-control", "none", "--kernel-name-base", "demangled", "-k", kregex, "-s", "1", "-c", "1",
+           "--csv", "--page", "raw"]
     cmd += ["--set", "full", "--metrics", METRICS] if full else ["--metrics", METRICS]
     cmd += [sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(cfg), "--steps", "1", "--warmup", "3",
             "--no-e2e", "--no-cpu-baseline", "--no-extras"]
@@ -39,7 +41,7 @@ def capture(cfg, algo_kind, full):
         i = hdr.index(name)
         v = float(vals[i].replace(",", ""))
         return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                    "msecond": 1e-3, "%": 1}.get(units[i], 1)
+                    "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1, "second": 1, "%": 1}.get(units[i], 1)
     rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
     dur = get("gpu__time_duration.sum")
     return kname, {"dram_bytes": int(rd + wr), "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
