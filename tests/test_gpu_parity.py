@@ -838,3 +838,27 @@ def test_tiled_bit_identical_and_preconditions():
         op.plan(64, "tiled")
     assert e.value.status == S.SPMM_ERR_UNSUPPORTED
     op.close()
+
+
+@pytest.mark.parametrize("algo", ["rowsplit", "merge", "tiled"])
+def test_execute_is_cuda_graph_capturable(algo):
+    """execute() enqueues only kernels / memsets on the given stream (no host sync, no allocation), so a
+    planned SpMM can be captured once in a CUDA graph and replayed on new B contents."""
+    p = synth.lognormal_rows(3000, 2000, 7.92, 17) if algo != "tiled" else synth.uniform_rows(800, 3000, 300, 4)
+    kind, n = "f32_plus_times", 64
+    val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n)
+    op = S.CsrSpmm(ro, ci, vd, p.k)
+    op.plan(n, algo)
+    op.execute(Bd, Cd)  # first launch outside the capture (kernel attributes, occupancy caches)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        op.execute(Bd, Cd)
+    for seed in (301, 302):
+        Bh2 = synth.dense(p.k, n, seed, kind)
+        Bd.copy_(Bh2.to(DEV))
+        Cd.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        check(p, kind, n, val, Bh2, Cd)
+    op.close()
