@@ -46,7 +46,8 @@ extern "C" {
  * need a 256-byte workspace (tile queue) -- callers must size the workspace from plan(); 4 = plan
  * option merge_worker (was reserved0), plan option tasks_per_warp (was reserved[0]) and
  * spmm_plan_info.merge_worker_lanes / tasks_per_warp (lane-folded merge, task queue),
- * spmm_csr_execute_ex (accumulate, peer copies of C) and the spmm_ipc_* buffers, SPMM_ALGO_TILED. */
+ * spmm_csr_execute_ex (accumulate, peer copies of C) and the spmm_ipc_* buffers, SPMM_ALGO_TILED,
+ * spmm_csr_multiply_host (host buffers). */
 #define SPMM_ABI_VERSION 4
 
 typedef struct spmm_csr_s* spmm_csr_t;
@@ -222,6 +223,24 @@ SPMM_API spmm_status spmm_csr_execute_ex(spmm_csr_t h, const void* B, int64_t ld
  *                   fails (SPMM_ERR_CUDA) for a handle exported by the calling process itself.
  *   spmm_ipc_close: unmap a pointer from spmm_ipc_open.
  */
+/*
+ * spmm_csr_multiply_host -- one-shot C = A (x) B on HOST buffers (the whole path behind one call):
+ * stream-ordered device buffers from a library-owned memory pool per device (kept across calls, so
+ * repeated calls reuse the memory and never synchronise the device), host->device copies of the CSR arrays and of columns [0, n) of B, create + plan
+ * (the given algo / semiring, AUTO policy) + execute, device->host copy of columns [0, n) of C (the
+ * host C's columns [n, ldc) are untouched), buffers released on the stream.  Host arrays: row_offsets
+ * [m+1], col_indices / values [nnz], B k x ldb, C m x ldc, row-major, 4-byte elements; pinned (page-
+ * locked) memory makes the copies asynchronous.  Plan synchronises `stream` once (the AUTO reduction);
+ * flags: SPMM_HOST_SYNC (1) also synchronises before return -- otherwise C is valid once `stream`
+ * completes, and the host arrays must stay valid until then.  Errors as create / plan / execute, plus
+ * SPMM_ERR_CUDA for a failed allocation or copy.
+ */
+enum { SPMM_HOST_SYNC = 1u };
+SPMM_API spmm_status spmm_csr_multiply_host(int64_t m, int64_t k, int64_t nnz, const int32_t* row_offsets,
+                                            const int32_t* col_indices, const void* values, spmm_dtype dtype,
+                                            const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
+                                            spmm_algo algo, spmm_semiring semiring, uint32_t flags, void* stream);
+
 /*
  * spmm_csr_split_columns -- set-up for the iterative distributed SpMM (NEXT-3): split every row of
  * A (m x ?, CSR, device) into the entries whose column lies in [c0, c1) and the others, keeping

@@ -43,7 +43,8 @@ struct spmm_csr_s {
     int32_t tl_kb = 0;            // tiled: B rows per shared-memory block
     int sorted = -1;              // column indices non-decreasing within rows: -1 unknown, 0 no, 1 yes
     size_t ws_bytes = 0;
-    int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags
+    int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags (stream-ordered allocation)
+    cudaStream_t st_alloc = nullptr;  // stream d_scratch was allocated on (freed on it: no device sync)
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
     int32_t nev = 0;
     std::string err;
@@ -444,7 +445,8 @@ spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, 
     if (!h) return SPMM_ERR_CUDA;
     h->m = m; h->k = k; h->nnz = nnz;
     h->ro = row_offsets; h->col = col_indices; h->val = values; h->dtype = dtype;
-    cudaError_t e = cudaMalloc(&h->d_scratch, 32);
+    h->st_alloc = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&h->d_scratch), 32, h->st_alloc);
     if (e != cudaSuccess) { delete h; return SPMM_ERR_CUDA; }
     if ((flags & SPMM_FLAG_VALIDATE) && m > 0) {
         cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -459,12 +461,12 @@ spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, 
         if (e == cudaSuccess) e = cudaMemcpyAsync(&hflags, h->d_scratch, sizeof(int), cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) {
-            cudaFree(h->d_scratch);
+            cudaFreeAsync(h->d_scratch, h->st_alloc);
             delete h;
             return SPMM_ERR_CUDA;
         }
         if (hflags) {
-            cudaFree(h->d_scratch);
+            cudaFreeAsync(h->d_scratch, h->st_alloc);
             delete h;
             return SPMM_ERR_INVALID_CSR;
         }
@@ -475,7 +477,7 @@ spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, 
 
 spmm_status spmm_csr_destroy(spmm_csr_t h) {
     if (!h) return SPMM_OK;
-    if (h->d_scratch) cudaFree(h->d_scratch);
+    if (h->d_scratch) cudaFreeAsync(h->d_scratch, h->st_alloc);  // stream-ordered: no device-wide sync
     delete h;
     return SPMM_OK;
 }
@@ -844,6 +846,77 @@ spmm_status spmm_merge_partition(const int32_t* row_offsets, int64_t m, int64_t 
     k_partition<<<(unsigned)pgrid, THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
         row_offsets, (int)m, (int)nnz, items_per_cta, partition, (int)num_ctas, states_out, nullptr);
     return cudaGetLastError() == cudaSuccess ? SPMM_OK : SPMM_ERR_CUDA;
+}
+
+// library-owned stream-ordered memory pool for spmm_csr_multiply_host (one per device, kept across
+// calls: a release threshold of "never" so repeated calls reuse the same device memory)
+static cudaMemPool_t host_api_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[8] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    cudaMemPool_t& p = pools[dev & 7];
+    if (!p) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) { p = nullptr; return nullptr; }
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    return p;
+}
+
+spmm_status spmm_csr_multiply_host(int64_t m, int64_t k, int64_t nnz, const int32_t* h_ro, const int32_t* h_col,
+                                   const void* h_val, spmm_dtype dtype, const void* h_B, int64_t ldb, void* h_C,
+                                   int64_t ldc, int32_t n, spmm_algo algo, spmm_semiring sr, uint32_t flags,
+                                   void* stream) {
+    if (m < 0 || k < 0 || nnz < 0 || n < 1 || ldb < n || ldc < n) return SPMM_ERR_INVALID_ARG;
+    if ((flags & ~SPMM_HOST_SYNC) != 0u) return SPMM_ERR_INVALID_ARG;
+    if (dtype != SPMM_F32 && dtype != SPMM_I32) return SPMM_ERR_INVALID_ARG;
+    if (m == 0) return SPMM_OK;
+    if (!h_ro || !h_C || (nnz > 0 && (!h_col || !h_val || !h_B))) return SPMM_ERR_NULL_POINTER;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t e4 = 4;
+    int32_t *d_ro = nullptr, *d_col = nullptr;
+    void *d_val = nullptr, *d_B = nullptr, *d_C = nullptr, *d_ws = nullptr;
+    spmm_csr_t h = nullptr;
+    spmm_status rc = SPMM_OK;
+    auto ok = [&](cudaError_t e) {
+        if (e != cudaSuccess && rc == SPMM_OK) rc = SPMM_ERR_CUDA;
+        return rc == SPMM_OK;
+    };
+    // stream-ordered device buffers from the library's pool (kept across calls: no device-wide sync)
+    cudaMemPool_t pool = host_api_pool();
+    if (!pool) return SPMM_ERR_CUDA;
+    auto dalloc = [&](void** ptr, size_t bytes) { return cudaMallocFromPoolAsync(ptr, bytes, pool, st); };
+    const size_t kk = (size_t)std::max<int64_t>(k, 1), zz = (size_t)std::max<int64_t>(nnz, 1);
+    if (ok(dalloc(reinterpret_cast<void**>(&d_ro), e4 * (size_t)(m + 1))) &&
+        ok(dalloc(reinterpret_cast<void**>(&d_col), e4 * zz)) && ok(dalloc(&d_val, e4 * zz)) &&
+        ok(dalloc(&d_B, e4 * kk * (size_t)n)) && ok(dalloc(&d_C, e4 * (size_t)m * (size_t)n)) &&
+        ok(cudaMemcpyAsync(d_ro, h_ro, e4 * (size_t)(m + 1), cudaMemcpyHostToDevice, st)) &&
+        (nnz == 0 || (ok(cudaMemcpyAsync(d_col, h_col, e4 * (size_t)nnz, cudaMemcpyHostToDevice, st)) &&
+                      ok(cudaMemcpyAsync(d_val, h_val, e4 * (size_t)nnz, cudaMemcpyHostToDevice, st)) &&
+                      ok(cudaMemcpy2DAsync(d_B, e4 * (size_t)n, h_B, e4 * (size_t)ldb, e4 * (size_t)n, (size_t)k,
+                                           cudaMemcpyHostToDevice, st))))) {
+        rc = spmm_csr_create(&h, m, k, nnz, d_ro, d_col, d_val, dtype, 0u, stream);
+        size_t ws = 0;
+        spmm_algo chosen;
+        if (rc == SPMM_OK) rc = spmm_csr_plan(h, n, algo, sr, 0.0, stream, &ws, &chosen);
+        if (rc == SPMM_OK && ws > 0) ok(dalloc(&d_ws, ws));
+        if (rc == SPMM_OK) rc = spmm_csr_execute(h, d_B, n, d_C, n, n, d_ws, ws, stream);
+        if (rc == SPMM_OK)  // columns [0, n) of C only: the host C's padding columns stay untouched
+            ok(cudaMemcpy2DAsync(h_C, e4 * (size_t)ldc, d_C, e4 * (size_t)n, e4 * (size_t)n, (size_t)m,
+                                 cudaMemcpyDeviceToHost, st));
+        if (h) spmm_csr_destroy(h);
+    }
+    for (void* p : {static_cast<void*>(d_ro), static_cast<void*>(d_col), d_val, d_B, d_C, d_ws})
+        if (p) cudaFreeAsync(p, st);
+    if (rc == SPMM_OK && (flags & SPMM_HOST_SYNC)) ok(cudaStreamSynchronize(st));
+    return rc;
 }
 
 spmm_status spmm_partition_rows(const int32_t* host_row_offsets, int64_t m, int32_t parts, int32_t mode,

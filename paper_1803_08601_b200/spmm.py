@@ -42,7 +42,8 @@ EXPORTED = ("spmm_csr_create", "spmm_csr_plan", "spmm_csr_plan_ex", "spmm_csr_ex
             "spmm_csr_destroy", "spmm_csr_get_plan_info", "spmm_status_string", "spmm_csr_last_error",
             "spmm_abi_version", "spmm_merge_num_ctas", "spmm_merge_partition", "spmm_partition_rows",
             "spmm_csr_set_timing_events", "spmm_csr_split_columns", "spmm_ipc_alloc", "spmm_ipc_free",
-            "spmm_ipc_open", "spmm_ipc_close")
+            "spmm_ipc_open", "spmm_ipc_close", "spmm_csr_multiply_host")
+SPMM_HOST_SYNC = 1
 SPMM_MAX_PEERS = 7
 SPMM_IPC_HANDLE_BYTES = 64
 
@@ -100,6 +101,8 @@ def load(path: str | None = None):
     lib.spmm_csr_split_columns.argtypes = [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32, c_int32, c_int32,
                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                            POINTER(c_int64), c_void_p]
+    lib.spmm_csr_multiply_host.argtypes = [c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
+                                           c_int64, c_void_p, c_int64, c_int32, c_int32, c_int32, c_uint32, c_void_p]
     lib.spmm_ipc_alloc.argtypes = [c_size_t, POINTER(c_void_p), c_void_p]
     lib.spmm_ipc_free.argtypes = [c_void_p]
     lib.spmm_ipc_open.argtypes = [c_void_p, POINTER(c_void_p)]
@@ -183,6 +186,31 @@ def spmm_csr_split_columns(ro_ptr, col_ptr, val_ptr, m, nnz, c0, c1, dtype, ro_i
     st = load().spmm_csr_split_columns(ro_ptr, col_ptr, val_ptr, m, nnz, c0, c1, dtype, ro_in, col_in, val_in, ro_out,
                                        col_out, val_out, ctypes.byref(nnz_in), stream)
     return st, nnz_in.value
+
+
+def spmm_csr_multiply_host(m, k, nnz, ro_ptr, col_ptr, val_ptr, dtype, B_ptr, ldb, C_ptr, ldc, n, algo, semiring,
+                           flags=0, stream=None) -> int:
+    return load().spmm_csr_multiply_host(m, k, nnz, ro_ptr, col_ptr, val_ptr, dtype, B_ptr, ldb, C_ptr, ldc, n, algo,
+                                         semiring, flags, stream)
+
+
+def multiply_host(row_offsets, col_indices, values, k, B, C=None, algo="auto", semiring="plus_times", stream=None,
+                  sync=True):
+    """C = A (x) B with every array in (preferably pinned) HOST memory, through spmm_csr_multiply_host:
+    the library copies in, plans, executes and copies C back on `stream`."""
+    import torch
+    for t in (row_offsets, col_indices, values, B):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("multiply_host takes contiguous host tensors")
+    m, nnz, n = row_offsets.numel() - 1, col_indices.numel(), B.shape[1]
+    if C is None:
+        C = torch.empty(m, n, dtype=B.dtype, pin_memory=True)
+    st = spmm_csr_multiply_host(m, k, nnz, c_void_p(row_offsets.data_ptr()), c_void_p(col_indices.data_ptr()),
+                                c_void_p(values.data_ptr()), _dtype_code(values), c_void_p(B.data_ptr()), B.stride(0),
+                                c_void_p(C.data_ptr()), C.stride(0), n, ALGOS[algo], SEMIRINGS[semiring],
+                                SPMM_HOST_SYNC if sync else 0, _stream_ptr(stream))
+    _check(st)
+    return C
 
 
 def spmm_ipc_alloc(nbytes):

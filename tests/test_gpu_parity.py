@@ -862,3 +862,29 @@ def test_execute_is_cuda_graph_capturable(algo):
         torch.cuda.synchronize()
         check(p, kind, n, val, Bh2, Cd)
     op.close()
+
+
+@pytest.mark.parametrize("kind", synth.KINDS)
+@pytest.mark.parametrize("algo", ["auto", "rowsplit", "merge"])
+def test_multiply_host_buffers(kind, algo):
+    """spmm_csr_multiply_host: the whole path behind one C call on host buffers (pinned and pageable),
+    padding columns of the host C untouched."""
+    p = synth.lognormal_rows(3000, 2000, 7.92, 17)
+    n, ldb, ldc = 33, 37, 40
+    val = synth.values(p.nnz, 311, kind)
+    Bh = synth.dense(p.k, n, 312, kind, ld=ldb)
+    poison = float("nan") if kind.startswith("f32") else -(2**31)
+    for pinned in (True, False):
+        Ch = torch.full((p.m, ldc), poison, dtype=Bh.dtype)
+        args = [p.row_offsets.contiguous(), p.col_indices.contiguous(), val.contiguous(), Bh, Ch]
+        if pinned:
+            args = [t.pin_memory() for t in args]
+        sr = "plus_times" if kind.endswith("plus_times") else "min_plus"
+        st = S.spmm_csr_multiply_host(p.m, p.k, p.nnz, *[a.data_ptr() for a in args[:3]], S._dtype_code(val),
+                                      args[3].data_ptr(), ldb, args[4].data_ptr(), ldc, n, S.ALGOS[algo],
+                                      S.SEMIRINGS[sr], S.SPMM_HOST_SYNC, None)
+        assert st == S.SPMM_OK
+        check(p, kind, n, val, Bh, args[4])
+    C2 = S.multiply_host(p.row_offsets, p.col_indices, val, p.k, Bh[:, :n].contiguous(), algo=algo,
+                         semiring="plus_times" if kind.endswith("plus_times") else "min_plus")
+    check(p, kind, n, val, Bh, C2)
