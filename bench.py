@@ -645,7 +645,8 @@ def run_e2e_pipelined(args, p, vals, B, C, n, dev, sampler, flops_all, ro_h, col
     def step(k):
         S.multiply_host(ro_h, col_h, val_h, p.k, B_h, C_hs[k % 2], algo=args.algo, stream=streams[k % 2], sync=False)
 
-    step(0)  # warm-up (also primes the stream-ordered memory pool)
+    step(0)  # warm-up on both streams (primes the library's memory pool with one buffer set per stream)
+    step(1)
     torch.cuda.synchronize()
     steps = max(1, args.e2e_steps)
     sampler.start()

@@ -900,8 +900,9 @@ spmm_status spmm_csr_multiply_host(int64_t m, int64_t k, int64_t nnz, const int3
         ok(cudaMemcpyAsync(d_ro, h_ro, e4 * (size_t)(m + 1), cudaMemcpyHostToDevice, st)) &&
         (nnz == 0 || (ok(cudaMemcpyAsync(d_col, h_col, e4 * (size_t)nnz, cudaMemcpyHostToDevice, st)) &&
                       ok(cudaMemcpyAsync(d_val, h_val, e4 * (size_t)nnz, cudaMemcpyHostToDevice, st)) &&
-                      ok(cudaMemcpy2DAsync(d_B, e4 * (size_t)n, h_B, e4 * (size_t)ldb, e4 * (size_t)n, (size_t)k,
-                                           cudaMemcpyHostToDevice, st))))) {
+                      ok(ldb == n ? cudaMemcpyAsync(d_B, h_B, e4 * (size_t)k * (size_t)n, cudaMemcpyHostToDevice, st)
+                                  : cudaMemcpy2DAsync(d_B, e4 * (size_t)n, h_B, e4 * (size_t)ldb, e4 * (size_t)n,
+                                                      (size_t)k, cudaMemcpyHostToDevice, st))))) {
         rc = spmm_csr_create(&h, m, k, nnz, d_ro, d_col, d_val, dtype, 0u, stream);
         size_t ws = 0;
         spmm_algo chosen;
@@ -909,8 +910,9 @@ spmm_status spmm_csr_multiply_host(int64_t m, int64_t k, int64_t nnz, const int3
         if (rc == SPMM_OK && ws > 0) ok(dalloc(&d_ws, ws));
         if (rc == SPMM_OK) rc = spmm_csr_execute(h, d_B, n, d_C, n, n, d_ws, ws, stream);
         if (rc == SPMM_OK)  // columns [0, n) of C only: the host C's padding columns stay untouched
-            ok(cudaMemcpy2DAsync(h_C, e4 * (size_t)ldc, d_C, e4 * (size_t)n, e4 * (size_t)n, (size_t)m,
-                                 cudaMemcpyDeviceToHost, st));
+            ok(ldc == n ? cudaMemcpyAsync(h_C, d_C, e4 * (size_t)m * (size_t)n, cudaMemcpyDeviceToHost, st)
+                        : cudaMemcpy2DAsync(h_C, e4 * (size_t)ldc, d_C, e4 * (size_t)n, e4 * (size_t)n, (size_t)m,
+                                            cudaMemcpyDeviceToHost, st));
         if (h) spmm_csr_destroy(h);
     }
     for (void* p : {static_cast<void*>(d_ro), static_cast<void*>(d_col), d_val, d_B, d_C, d_ws})

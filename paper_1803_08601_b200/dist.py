@@ -286,14 +286,16 @@ class IterativeRowBlockSpmm:
     accumulate, spmm_csr_execute_ex).  Rows of C are independent, so the result equals the
     single-GPU product (fp32 up to summation order)."""
 
-    def __init__(self, row_offsets, col_indices, values, *, group=None, mode: int = 1, device=None,
-                 local_factory=None, split_fn=None):
+    def __init__(self, row_offsets, col_indices, values, k: int | None = None, *, group=None, mode: int = 1,
+                 device=None, local_factory=None, split_fn=None):
         import torch.distributed as dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.device = device or values.device
         self.m = row_offsets.numel() - 1
+        if k is not None and int(k) != self.m:
+            raise ValueError(f"iterative SpMM needs a square A (X and Y share the row blocks): m = {self.m}, k = {k}")
         self.bounds = partition_rows(row_offsets, self.world, mode)
         r0, r1 = self.bounds[self.rank], self.bounds[self.rank + 1]
         ro, col, val = slice_rows(row_offsets, col_indices, values, r0, r1)
