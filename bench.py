@@ -430,11 +430,20 @@ def main():
     # ---------------- e2e: host buffers through the public API ----------------
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, ctx, n, world, rank, dev, sampler, head["flops_all"], distributed)
+        if distributed:
+            e2e = run_e2e(args, ctx, n, world, rank, dev, sampler, head["flops_all"], distributed)
+        else:
+            # one GPU: host copies of the step's inputs, then the device-resident workload is released
+            # (the library's own pool holds the e2e device buffers, one set per stream in flight)
+            host = e2e_host_inputs(ctx, n)
+            ctx[4].close()
+            ctx = None
+            torch.cuda.empty_cache()
+            e2e = run_e2e_pipelined(args, host, n, dev, sampler, head["flops_all"])
     # ---------------- extra configs in the same process (one GPU) ----------------
     extras = {}
     if not distributed and not args.no_extras:
-        del ctx
+        ctx = None
         torch.cuda.empty_cache()
         for cfg in (1, 2):
             if cfg == args.config:
@@ -586,9 +595,6 @@ def run_e2e(args, ctx, n, world, rank, dev, sampler, flops_all, distributed):
     C_h = torch.empty(p.m, n, dtype=torch.float32, pin_memory=True)
     h2d = ro_h.numel() * 4 + col_h.numel() * 4 + val_h.numel() * 4 + (B_h.numel() * 4 if B_h is not None else 0)
     d2h = C_h.numel() * 4
-    if not distributed:
-        return run_e2e_pipelined(args, p, vals, B, C, n, dev, sampler, flops_all, ro_h, col_h, val_h, B_h, C_h,
-                                 None, h2d, d2h)
     ro_d, col_d, val_d = torch.empty_like(p.row_offsets), torch.empty_like(p.col_indices), torch.empty_like(vals)
     B_d = B  # reuse the device allocation (its contents are overwritten by the H2D copy / broadcast)
     C_d = C
@@ -632,18 +638,27 @@ def run_e2e(args, ctx, n, world, rank, dev, sampler, flops_all, distributed):
                         (" + NCCL broadcast of B" if distributed else "")}
 
 
-def run_e2e_pipelined(args, p, vals, B, C, n, dev, sampler, flops_all, ro_h, col_h, val_h, B_h, C_h, dev_csr,
-                      h2d, d2h):
+def e2e_host_inputs(ctx, n):
+    """Pinned host copies of one step's inputs (CSR + B) and two pinned C buffers."""
+    p, vals, B, C, _ = ctx
+    return {"m": p.m, "k": p.k, "ro": p.row_offsets.cpu().pin_memory(), "col": p.col_indices.cpu().pin_memory(),
+            "val": vals.cpu().pin_memory(), "B": B.cpu().pin_memory(),
+            "C": [torch.empty(p.m, n, dtype=torch.float32, pin_memory=True) for _ in range(2)]}
+
+
+def run_e2e_pipelined(args, host, n, dev, sampler, flops_all):
     """One GPU: every step is ONE C-ABI call on pinned HOST buffers (spmm_csr_multiply_host: the library
     copies the CSR and B in, creates + plans + executes, copies C out; stream-ordered device buffers).
     Steps alternate between two streams, so step k's host->device copies overlap step k-1's read-back
     (PCIe is full duplex), as a serving loop would run them; each step still moves all of its bytes."""
     from paper_1803_08601_b200 import spmm as S
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-    C_hs = [C_h, torch.empty(C_h.shape, dtype=C_h.dtype, pin_memory=True)]
+    h2d = 4 * (host["ro"].numel() + host["col"].numel() + host["val"].numel() + host["B"].numel())
+    d2h = 4 * host["C"][0].numel()
 
     def step(k):
-        S.multiply_host(ro_h, col_h, val_h, p.k, B_h, C_hs[k % 2], algo=args.algo, stream=streams[k % 2], sync=False)
+        S.multiply_host(host["ro"], host["col"], host["val"], host["k"], host["B"], host["C"][k % 2], algo=args.algo,
+                        stream=streams[k % 2], sync=False)
 
     step(0)  # warm-up on both streams (primes the library's memory pool with one buffer set per stream)
     step(1)

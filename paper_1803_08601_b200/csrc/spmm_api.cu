@@ -45,6 +45,7 @@ struct spmm_csr_s {
     size_t ws_bytes = 0;
     int* d_scratch = nullptr;  // 32 bytes: plan-time reductions / validation flags (stream-ordered allocation)
     cudaStream_t st_alloc = nullptr;  // stream d_scratch was allocated on (freed on it: no device sync)
+    int64_t hint_max_row = -1;        // longest row when known on the host (skips plan's device reduction)
     cudaEvent_t ev[8] = {};    // optional per-kernel timing events (spmm_csr_set_timing_events)
     int32_t nev = 0;
     std::string err;
@@ -520,7 +521,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
     h->sr = sr;
     h->mfold = fold;
     h->mdyn = false;
-    h->max_row = -1;
+    h->max_row = h->hint_max_row;  // -1 unless the caller already knows it (spmm_csr_multiply_host)
     h->capb = 0;
     h->bspan_compact = -1.0;
     h->rs_dyn = false;
@@ -536,8 +537,10 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             // kernel handles short rows well, so the row-length threshold is replaced by the two causes of
             // Type 1 imbalance that merge path removes: a skewed row-length
             // distribution, or too few rows to fill the GPU's row groups.
-            const spmm_status ms = measure_max_row(h, stream);
-            if (ms != SPMM_OK) return ms;
+            if (h->max_row < 0) {
+                const spmm_status ms = measure_max_row(h, stream);
+                if (ms != SPMM_OK) return ms;
+            }
             const long long hmax = h->max_row;
             const bool skewed = (double)hmax > 16.0 * d && hmax >= 1024;
             const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true);
@@ -866,6 +869,10 @@ static cudaMemPool_t host_api_pool() {
         if (cudaMemPoolCreate(&p, &props) != cudaSuccess) { p = nullptr; return nullptr; }
         uint64_t keep = UINT64_MAX;
         cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+        // never make a call on one stream wait for memory another stream is still using: the pool grows
+        // to one buffer set per stream in flight instead, and calls on different streams overlap
+        int no = 0;
+        cudaMemPoolSetAttribute(p, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     return p;
 }
@@ -904,6 +911,13 @@ spmm_status spmm_csr_multiply_host(int64_t m, int64_t k, int64_t nnz, const int3
                                   : cudaMemcpy2DAsync(d_B, e4 * (size_t)n, h_B, e4 * (size_t)ldb, e4 * (size_t)n,
                                                       (size_t)k, cudaMemcpyHostToDevice, st))))) {
         rc = spmm_csr_create(&h, m, k, nnz, d_ro, d_col, d_val, dtype, 0u, stream);
+        // the longest row from the host copy (while the copies above are in flight): plan then needs no
+        // device reduction + read-back, so the call does not wait on this stream's copies
+        if (rc == SPMM_OK) {
+            int32_t mx = 0;
+            for (int64_t i = 0; i < m; ++i) mx = std::max(mx, h_ro[i + 1] - h_ro[i]);
+            h->hint_max_row = mx;
+        }
         size_t ws = 0;
         spmm_algo chosen;
         if (rc == SPMM_OK) rc = spmm_csr_plan(h, n, algo, sr, 0.0, stream, &ws, &chosen);
