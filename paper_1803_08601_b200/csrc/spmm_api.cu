@@ -1,6 +1,7 @@
 // spmm_api.cu -- the C ABI of libspmm.so (include/spmm.h): handle, planner, §5.4 heuristic,
 // workspace sizing, argument checks and kernel dispatch for the sm_100a CSR SpMM kernels.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -14,6 +15,15 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "merge.cuh"
+
+namespace {
+// NVTX range around each C-ABI call (create / plan / execute / multiply_host), visible to nsys / ncu
+// --nvtx; header-only NVTX v3: a no-op function-pointer call when no tool is attached
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace spmm;
 
@@ -432,6 +442,7 @@ const char* spmm_csr_last_error(spmm_csr_t h) {
 spmm_status spmm_csr_create(spmm_csr_t* out, int64_t m, int64_t k, int64_t nnz, const int32_t* row_offsets,
                             const int32_t* col_indices, const void* values, spmm_dtype dtype, uint32_t flags,
                             void* stream) {
+    NvtxRange nvtx_range("spmm_csr_create");
     if (!out) return SPMM_ERR_NULL_POINTER;
     *out = nullptr;
     if (m < 0 || k < 0 || nnz < 0 || m >= 0x7fffffffLL || k >= 0x7fffffffLL || nnz >= 0x7fffffffLL ||
@@ -492,6 +503,7 @@ int64_t spmm_merge_num_ctas(int64_t m, int64_t nnz, int32_t items_per_cta, int32
 
 spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semiring sr, double threshold,
                              const spmm_plan_opts* opts, void* stream, size_t* workspace_bytes, spmm_algo* chosen) {
+    NvtxRange nvtx_range("spmm_csr_plan");
     if (!h) return SPMM_ERR_NULL_POINTER;
     h->planned = false;
     if (n < 1) return fail(h, SPMM_ERR_INVALID_ARG, "n must be >= 1");
@@ -733,6 +745,7 @@ spmm_status spmm_csr_get_plan_info(spmm_csr_t h, spmm_plan_info* out) {
 
 spmm_status spmm_csr_execute_ex(spmm_csr_t h, const void* B, int64_t ldb, void* C, int64_t ldc, int32_t n,
                                 void* workspace, size_t workspace_bytes, const spmm_exec_opts* opts, void* stream) {
+    NvtxRange nvtx_range("spmm_csr_execute");
     if (!h) return SPMM_ERR_NULL_POINTER;
     if (!h->planned) return fail(h, SPMM_ERR_NOT_PLANNED, "execute before plan");
     if (n != h->n) return fail(h, SPMM_ERR_INVALID_ARG, "n differs from the planned n");
@@ -881,6 +894,7 @@ spmm_status spmm_csr_multiply_host(int64_t m, int64_t k, int64_t nnz, const int3
                                    const void* h_val, spmm_dtype dtype, const void* h_B, int64_t ldb, void* h_C,
                                    int64_t ldc, int32_t n, spmm_algo algo, spmm_semiring sr, uint32_t flags,
                                    void* stream) {
+    NvtxRange nvtx_range("spmm_csr_multiply_host");
     if (m < 0 || k < 0 || nnz < 0 || n < 1 || ldb < n || ldc < n) return SPMM_ERR_INVALID_ARG;
     if ((flags & ~SPMM_HOST_SYNC) != 0u) return SPMM_ERR_INVALID_ARG;
     if (dtype != SPMM_F32 && dtype != SPMM_I32) return SPMM_ERR_INVALID_ARG;
