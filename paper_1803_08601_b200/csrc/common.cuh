@@ -142,36 +142,4 @@ __device__ __forceinline__ void epi_store(const EpiParams& E, T* C, long long ld
     else st_vec<VEC>(p, o);
 }
 
-// ---------------------------------------------------------------------------------------------
-// Warp-cooperative 32-ary search: first x in [lo, hi) with pred(x) true (pred monotone
-// false..true), or hi if none.  ~log32(hi-lo) rounds of one coalesced-ish probe per lane.
-// All 32 lanes must call it with identical arguments.
-// ---------------------------------------------------------------------------------------------
-template <class Pred>
-__device__ __forceinline__ long long warp_search_first(long long lo, long long hi, Pred pred) {
-    const int lane = threadIdx.x & 31;
-    while (hi - lo > 32) {
-        const long long step = (hi - lo + 31) / 32;
-        const long long x = lo + lane * step;
-        const bool p = (x >= hi) || pred(x);
-        const unsigned b = __ballot_sync(FULL, p);
-        if (b == 0u) {
-            lo = lo + 31 * step + 1;
-        } else {
-            const int f = __ffs(b) - 1;
-            if (f == 0) {
-                hi = lo;
-            } else {
-                const long long xf = lo + f * step;
-                lo = lo + (long long)(f - 1) * step + 1;
-                hi = xf < hi ? xf : hi;
-            }
-        }
-    }
-    const long long x = lo + lane;
-    const bool p = (x >= hi) || pred(x);
-    const unsigned b = __ballot_sync(FULL, p);
-    return b ? lo + (__ffs(b) - 1) : hi;
-}
-
 }  // namespace spmm

@@ -13,6 +13,9 @@
 #ifndef RS_U
 #define RS_U 8  // row split: B rows gathered back to back per row group
 #endif
+#ifndef RS_U4
+#define RS_U4 4  // row split, 4 float4 blocks per lane (n > 96): B rows gathered back to back per row group
+#endif
 #ifndef MW_U
 #define MW_U 8  // merge: B rows gathered per batch (row of <= 2 values per lane)
 #endif

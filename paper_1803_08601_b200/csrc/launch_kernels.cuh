@@ -53,11 +53,12 @@ cudaError_t launch_tile(const TileParams& P, cudaStream_t st) {
 
 template <typename T, int SR>
 cudaError_t rowsplit_kernel(VecCfg cfg, const TileParams& P, cudaStream_t st) {
-#define RS_CASE(V, G_, NV_) \
-    case (V)*1000 + (G_)*10 + (NV_): return launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, RS_U>(P, st);
+#define RS_CASE_U(V, G_, NV_, U_) \
+    case (V)*1000 + (G_)*10 + (NV_): return launch_tile<T, SR, MODE_ROWSPLIT, V, G_, NV_, U_>(P, st);
+#define RS_CASE(V, G_, NV_) RS_CASE_U(V, G_, NV_, RS_U)
     switch (cfg.vec * 1000 + cfg.G * 10 + cfg.NV) {
         RS_CASE(4, 1, 1) RS_CASE(4, 2, 1) RS_CASE(4, 4, 1) RS_CASE(4, 8, 1) RS_CASE(4, 8, 2) RS_CASE(4, 16, 2)
-        RS_CASE(4, 4, 4) RS_CASE(4, 8, 4)
+        RS_CASE(4, 4, 4) RS_CASE_U(4, 8, 4, RS_U4)
         RS_CASE(2, 1, 1) RS_CASE(2, 2, 1) RS_CASE(2, 4, 1) RS_CASE(2, 8, 1) RS_CASE(2, 8, 2) RS_CASE(2, 16, 2)
         RS_CASE(2, 32, 2)
         RS_CASE(1, 1, 1) RS_CASE(1, 2, 1) RS_CASE(1, 4, 1) RS_CASE(1, 8, 1) RS_CASE(1, 8, 2) RS_CASE(1, 16, 2)
@@ -65,6 +66,7 @@ cudaError_t rowsplit_kernel(VecCfg cfg, const TileParams& P, cudaStream_t st) {
         default: return cudaErrorNotSupported;
     }
 #undef RS_CASE
+#undef RS_CASE_U
 }
 
 // launch of a warp-task merge kernel (k_merge_w / k_merge_f): persistent grid of resident CTAs x SMs,

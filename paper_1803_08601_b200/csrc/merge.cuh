@@ -6,7 +6,7 @@
 //   merge of row-end offsets with nonzero indices (rows first on ties), so every task gets I items =
 //   rows + nonzeros, which also charges the C write of empty rows.  1-D nonzero split
 //   (PAPER.md:80, the paper's own choice, :89): task c starts at nonzero c*I in the largest row r with
-//   ro[r] <= c*I.  One warp per boundary, 32-ary search (~6 dependent probes).
+//   ro[r] <= c*I.  One coalesced pass over the rows: each row writes the boundaries that fall inside it.
 // Phase 2 (Alg. 1 lines 3-23) is k_merge_w in merge_w.cuh: each warp streams its tasks' items from
 //   global memory through small windows (the GlobalToShared of line 5 becomes a per-warp cp.async
 //   window), with a running accumulator flushed on each row end; a task's open row becomes its
@@ -20,89 +20,157 @@
 
 namespace spmm {
 
-// merge-path predicate: row end of row x (at path position x + ro[x+1]) lies before diagonal D
-struct MergePred {
-    const int* ro;
-    long long D;
-    __device__ __forceinline__ bool operator()(long long x) const {
-        return (long long)ld_stream(ro + x + 1) > D - x - 1;
-    }
-};
-struct NzPred {  // first r with ro[r] > t
-    const int* ro;
-    long long t;
-    __device__ __forceinline__ bool operator()(long long x) const { return (long long)ld_stream(ro + x) > t; }
-};
-
-// states[2c] = row, states[2c+1] = nonzero, c in [0, num_ctas]
+// states[2c] = row, states[2c+1] = nonzero, c in [0, num_ctas]: one pass over the rows instead of a
+// search per boundary.  2-D merge path: the row-end item of row r sits at path position
+// p_r = r + ro[r+1] (rows first on ties), so the boundary on diagonal d = c*I (< m + nnz) has consumed
+// exactly the rows with p_r < d, i.e. row r for p_{r-1} < d <= p_r, and nonzero d - r (the oracle's
+// characterisation, tests/test_oracle.py).  1-D nonzero split: the boundary at nonzero t = c*I lies in
+// the non-empty row r with ro[r] <= t < ro[r+1] (the largest r with ro[r] <= t).  Boundary 0 is
+// (0, 0) and boundary num_ctas is (m, nnz) in both.  Thread r reads ro[r], ro[r+1] (coalesced) and
+// writes the boundaries inside its row -- usually none or one; a row longer than I owns several.
+// It also zeroes the compute kernel's task queue.
 __global__ void __launch_bounds__(THREADS)
 k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states,
             int* __restrict__ task_ctr) {
-    const int lane = threadIdx.x & 31;
-    if (task_ctr && blockIdx.x == 0 && threadIdx.x == 0) *task_ctr = 0;  // the compute kernel's task queue
-    const long long c = (long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
-    if (c > num_ctas) return;
-    long long row, nz;
-    if (mode == 0) {
-        const long long D = min(c * items, (long long)m + nnz);
-        const long long lo = max(0LL, D - nnz), hi = min(D, (long long)m);
-        row = warp_search_first(lo, hi, MergePred{ro, D});
-        nz = D - row;
-    } else {
-        if (c == 0) {
-            row = 0; nz = 0;
-        } else if (c == num_ctas) {
-            row = m; nz = nnz;
-        } else {
-            const long long t = c * items;  // < nnz
-            row = warp_search_first(0, (long long)m + 1, NzPred{ro, t}) - 1;
-            nz = t;
-        }
+    const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid0 == 0) {
+        if (task_ctr) *task_ctr = 0;
+        states[0] = 0;
+        states[1] = 0;
+        states[2LL * num_ctas] = m;
+        states[2LL * num_ctas + 1] = nnz;
     }
-    if (lane == 0) {
-        states[2 * c] = (int)row;
-        states[2 * c + 1] = (int)nz;
+    const long long I = items;
+    const long long last = (long long)num_ctas - 1;  // interior boundaries 1 .. num_ctas - 1
+    const long long stride = 4LL * gridDim.x * blockDim.x;
+    // 4 consecutive rows per thread and iteration: the 5 row offsets they need are loaded back to back
+    // (one memory round trip per iteration; lanes cover 4 x 32 consecutive rows)
+    for (long long r0 = 4 * tid0; r0 < m; r0 += stride) {
+        int o[5];
+#pragma unroll
+        for (int u = 0; u < 5; ++u) o[u] = (r0 + u <= m) ? __ldg(ro + r0 + u) : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long r = r0 + u;
+            if (r >= m) break;
+            const long long a = o[u], b = o[u + 1];
+            long long c_lo, c_hi, base;
+            if (mode == 0) {
+                c_lo = (r - 1 + a) / I + 1;  // first c with c*I > p_{r-1} (p_{-1} = -1)
+                c_hi = (r + b) / I;          // last c with c*I <= p_r
+                base = -r;                   // nonzero = c*I - r
+            } else {
+                if (a >= b) continue;        // empty rows hold no nonzero boundary
+                c_lo = (a + I - 1) / I;
+                c_hi = (b - 1) / I;
+                base = 0;                    // nonzero = c*I
+            }
+            if (c_lo < 1) c_lo = 1;
+            if (c_hi > last) c_hi = last;
+            for (long long c = c_lo; c <= c_hi; ++c) {
+                states[2 * c] = (int)r;
+                states[2 * c + 1] = (int)(c * I + base);
+            }
+        }
     }
 }
 
-// FixCarryOut (Alg. 1 line 24): one warp per task carry; the first task of each run of equal carry
-// rows sums the run in ascending task order and adds it into C[row].
+// grid of k_partition: 4 rows per thread and iteration, at most 8 CTAs per SM
+inline unsigned partition_grid(long long m) {
+    const long long g = (m + 4LL * THREADS - 1) / (4LL * THREADS);
+    return (unsigned)(g < 1 ? 1 : (g > 8LL * 148 ? 8LL * 148 : g));
+}
+
+// FixCarryOut (Alg. 1 line 24): the first task of each run of equal carry rows sums the run in
+// ascending task order and adds it into C[row].  One warp per FIX_K consecutive carries, lanes over
+// columns: every load of the common case (runs of one carry) is issued before the first use, so the
+// kernel costs two memory round trips (carries, then the C rows) instead of one chain per carry.
+// (Carry values are read even when their flag is 0 -- workspace memory, never used then.)
+constexpr int FIX_K = 4;
+inline unsigned fixup_grid(long long num_ctas) {
+    return (unsigned)((num_ctas + (long long)FIX_K * WARPS_PER_CTA - 1) / ((long long)FIX_K * WARPS_PER_CTA));
+}
 template <typename T, int SR>
 __global__ void __launch_bounds__(THREADS)
 k_fixup(int num_ctas, int n, const int* __restrict__ carry_row, const int* __restrict__ carry_flag,
         const T* __restrict__ carry_val, T* __restrict__ C, long long ldc, const EpiParams E) {
     using R = Ring<T, SR>;
     const int lane = threadIdx.x & 31;
-    const long long c = (long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5);
-    if (c >= num_ctas) return;
-    const int row = carry_row[c];
-    if (row < 0) return;
-    if (c > 0 && carry_row[c - 1] == row) return;  // not the head of its run
-    T s[4];
+    const long long c0 = ((long long)blockIdx.x * WARPS_PER_CTA + (threadIdx.x >> 5)) * FIX_K;
+    if (c0 >= num_ctas) return;
+    int rw[FIX_K + 2];  // carry rows of tasks c0 - 1 .. c0 + FIX_K (-1: none)
 #pragma unroll
-    for (int t = 0; t < 4; ++t) s[t] = R::id();
-    bool any = false;
-    for (long long cc = c; cc < num_ctas && carry_row[cc] == row; ++cc) {
-        if (carry_flag[cc]) {
-            any = true;
+    for (int i = 0; i < FIX_K + 2; ++i) {
+        const long long cc = c0 - 1 + i;
+        rw[i] = (cc >= 0 && cc < num_ctas) ? carry_row[cc] : -1;
+    }
+    int fl[FIX_K];
+    T s[FIX_K][4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const int j = lane + 32 * t;
-                if (j < n) s[t] = R::add(s[t], carry_val[cc * n + j]);
-            }
+    for (int k = 0; k < FIX_K; ++k) {
+        const long long cc = c0 + k;
+        fl[k] = cc < num_ctas ? carry_flag[cc] : 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int j = lane + 32 * t;
+            s[k][t] = (cc < num_ctas && j < n) ? carry_val[cc * n + j] : R::id();
         }
     }
-    if (!any) return;
-    // C[row] (+)= the run (the owner's write, already accumulated into C if requested, came first); the
-    // final row also goes to the peer copies of C
-    T* crow = C + (long long)row * ldc;
+    bool head[FIX_K];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        const int j = lane + 32 * t;
-        if (j < n) {
-            const T v = R::add(crow[j], s[t]);
-            crow[j] = v;
-            for (int i = 0; i < E.npeers; ++i) static_cast<T*>(E.peer[i])[(row + E.peer_row0) * E.peer_ldc + j] = v;
+    for (int k = 0; k < FIX_K; ++k) {
+        const int row = rw[k + 1];
+        bool any = fl[k] != 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) s[k][t] = any ? R::add(R::id(), s[k][t]) : R::id();
+        head[k] = row >= 0 && rw[k] != row;  // the first carry of its run
+        if (head[k] && rw[k + 2] == row) {  // a run of several carries (a row spanning > 2 tasks; warp-uniform)
+            // 32 carries per round: lanes load their row / flag, a ballot finds where the run ends, then
+            // the flagged partials are added in ascending task order (their loads are independent)
+            for (long long cc = c0 + k + 1;; cc += 32) {
+                const long long cl = cc + lane;
+                const int rl = cl < num_ctas ? carry_row[cl] : -1;
+                const int fg = cl < num_ctas ? carry_flag[cl] : 0;
+                const unsigned same = __ballot_sync(FULL, rl == row);
+                const int len = (same == FULL) ? 32 : __ffs(~same) - 1;  // run members in this round
+                unsigned fm = __ballot_sync(FULL, fg != 0) & (len == 32 ? FULL : ((1u << len) - 1u));
+                any = any || fm != 0u;
+#pragma unroll 4
+                for (; fm; fm &= fm - 1u) {
+                    const long long cf = cc + (__ffs(fm) - 1);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int j = lane + 32 * t;
+                        if (j < n) s[k][t] = R::add(s[k][t], carry_val[cf * n + j]);
+                    }
+                }
+                if (len < 32) break;
+            }
+        }
+        head[k] = head[k] && any;
+    }
+    // C[row] (+)= the run (the owner's write, already accumulated into C if requested, came first); the
+    // final row also goes to the peer copies of C.  All C rows are read before the first store.
+    T cv[FIX_K][4];
+#pragma unroll
+    for (int k = 0; k < FIX_K; ++k)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int j = lane + 32 * t;
+            cv[k][t] = (head[k] && j < n) ? C[(long long)rw[k + 1] * ldc + j] : R::id();
+        }
+#pragma unroll
+    for (int k = 0; k < FIX_K; ++k) {
+        if (!head[k]) continue;
+        const long long row = rw[k + 1];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int j = lane + 32 * t;
+            if (j < n) {
+                const T v = R::add(cv[k][t], s[k][t]);
+                C[row * ldc + j] = v;
+                for (int i = 0; i < E.npeers; ++i) static_cast<T*>(E.peer[i])[(row + E.peer_row0) * E.peer_ldc + j] = v;
+            }
         }
     }
 }

@@ -207,7 +207,9 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
         // column blocks each (n = 64: 8 lanes x 2 float4) -- more rows per warp, fewer broadcast loads
         const int G0 = std::min(32, pow2ceil(lanes));
         if (lanes <= 32 && G0 >= 16) {
-            c.G = G0 / RS_GDIV;
+            // n = 97..128 with float4: 8 lanes x 4 blocks (4 rows per warp; measured 3% faster than 16 x 2
+            // on banded n = 128, profiles/r02_s3_experiments.txt); n = 64: 8 lanes x 2 blocks (4 x 4 slower)
+            c.G = (G0 == 32 && vec == 4 && lanes > 24) ? 8 : G0 / RS_GDIV;
             c.NV = (lanes + c.G - 1) / c.G;
         } else {
             c.G = G0;
@@ -262,7 +264,11 @@ VecCfg pick_fold(int n, const void* B, int64_t ldb, const void* C, int64_t ldc) 
 }
 
 // tiled kernel row groups: float4 over n (n % 4 == 0), G lanes x NV blocks as the row split picks them
-VecCfg tiled_cfg(int n) { return pick_vec(n, nullptr, 4, nullptr, 4, true); }
+VecCfg tiled_cfg(int n) {  // the tiled kernel keeps 16-lane groups at n > 96
+    VecCfg c = pick_vec(n, nullptr, 4, nullptr, 4, true);
+    if (c.G == 8 && c.NV == 4) { c.G = 16; c.NV = 2; }
+    return c;
+}
 bool tiled_shape_ok(int n) {
     if (n % 4 != 0 || n < 32 || n > 128) return false;
     const VecCfg c = tiled_cfg(n);
@@ -302,9 +308,8 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     int* task_ctr = h->mdyn ? reinterpret_cast<int*>(ws + off) : nullptr;  // zeroed by k_partition
     const int items = h->items;
     // phase 1: PartitionSpmm (Alg. 1 line 2)
-    const long long pgrid = (NC + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
     mark(h, 0, st);
-    k_partition<<<(unsigned)pgrid, THREADS, 0, st>>>(h->ro, (int)h->m, (int)h->nnz, items, h->opts.partition, (int)NC,
+    k_partition<<<partition_grid(h->m), THREADS, 0, st>>>(h->ro, (int)h->m, (int)h->nnz, items, h->opts.partition, (int)NC,
                                                      states, task_ctr);
     mark(h, 1, st);
     cudaError_t e = cudaGetLastError();
@@ -325,8 +330,7 @@ cudaError_t launch_merge(const spmm_csr_s* h, VecCfg cfg, TileParams P, unsigned
     mark(h, 2, st);
     if (e != cudaSuccess) return e;
     // phase 3: FixCarryOut (Alg. 1 line 24)
-    const long long fgrid = (NC + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-    k_fixup<T, SR><<<(unsigned)fgrid, THREADS, 0, st>>>((int)NC, h->n, carry_row, carry_flag, carry_val,
+    k_fixup<T, SR><<<fixup_grid(NC), THREADS, 0, st>>>((int)NC, h->n, carry_row, carry_flag, carry_val,
                                                         static_cast<T*>(P.C), P.ldc, P.epi);
     mark(h, 3, st);
     return cudaGetLastError();
@@ -858,8 +862,7 @@ spmm_status spmm_merge_partition(const int32_t* row_offsets, int64_t m, int64_t 
     if (items_per_cta <= 0 || m < 0 || nnz < 0 || m + nnz >= 0x7fffffffLL) return SPMM_ERR_INVALID_ARG;
     if (num_ctas != spmm_merge_num_ctas(m, nnz, items_per_cta, partition)) return SPMM_ERR_INVALID_ARG;
     if (num_ctas == 0) return SPMM_OK;
-    const long long pgrid = (num_ctas + 1 + WARPS_PER_CTA - 1) / WARPS_PER_CTA;
-    k_partition<<<(unsigned)pgrid, THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+    k_partition<<<partition_grid(m), THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
         row_offsets, (int)m, (int)nnz, items_per_cta, partition, (int)num_ctas, states_out, nullptr);
     return cudaGetLastError() == cudaSuccess ? SPMM_OK : SPMM_ERR_CUDA;
 }
