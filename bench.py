@@ -180,7 +180,14 @@ def load_traffic(key: str, sha: str | None):
     if not isinstance(ent, dict):
         ent = {"dram_bytes": ent}
     ent = dict(ent)
-    ent["same_build"] = (ent.get("lib_sha16") == sha) if sha else None
+    # same build = the same .so, or the same sources and flags (nvcc builds are not bit-reproducible:
+    # paper_1803_08601_b200.build.source_sha16); a variant library (SPMM_LIB) matches only by its hash
+    same_lib = (ent.get("lib_sha16") == sha) if sha else None
+    same_src = None
+    if not os.environ.get("SPMM_LIB") and ent.get("src_sha16"):
+        from paper_1803_08601_b200 import build as _build
+        same_src = ent["src_sha16"] == _build.source_sha16()
+    ent["same_build"] = bool(same_lib or same_src) if (same_lib is not None or same_src is not None) else None
     return ent
 
 

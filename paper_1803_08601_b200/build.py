@@ -31,6 +31,21 @@ def _nvcc() -> str:
     return "nvcc"
 
 
+def source_sha16(defines=()) -> str:
+    """Identity of a build from its inputs: sha256 over every source / header the library is built from,
+    the nvcc flags and extra defines.  (The .so itself is not bit-reproducible: nvcc names internal-
+    linkage device symbols after the compiling process, so two builds of the same sources differ in a
+    few symbol-name bytes while their SASS is identical.)"""
+    import hashlib
+    h = hashlib.sha256()
+    for d in sorted(DEPS):
+        h.update(os.path.relpath(d, ROOT).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(NVCC_FLAGS + [f"-D{d}" for d in defines]).encode())
+    return h.hexdigest()[:16]
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True

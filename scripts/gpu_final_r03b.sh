@@ -6,6 +6,7 @@ O=gpurun_out/final3
 mkdir -p $O
 sha256sum paper_1803_08601_b200/libspmm.so | cut -c1-16 > $O/lib_sha16_b.txt
 O=$O bash scripts/gpu_sanitize.sh
+timeout 3000 python scripts/ncu_traffic.py $O/ncu_traffic_b.json > $O/ncu_traffic_b.log 2>&1; echo "ncu_traffic b rc=$?"
 timeout 3000 python scripts/sweep_config4.py --out $O/config3 > $O/config3.log 2>&1; echo "config3 rc=$?"
 tail -8 $O/config3.log
 timeout 2400 python scripts/scaling_emulation.py --config 4 --out $O/scaling_emulation_config4 > $O/scaling4.log 2>&1; echo "scaling rc=$?"

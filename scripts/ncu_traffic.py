@@ -54,10 +54,14 @@ def capture(cfg, algo_kind, full):
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "ncu_traffic.json")
     sha = sha16()
+    sys.path.insert(0, ROOT)
+    from paper_1803_08601_b200 import build as B
+    src = B.source_sha16()
     res = {}
     for cfg, algo, full in ((1, "rowsplit", True), (2, "merge", True), (4, "merge", False)):
         kname, ent = capture(cfg, algo, full)
         ent["lib_sha16"] = sha
+        ent["src_sha16"] = src
         res[f"config{cfg}_n64|{kname}"] = ent
         print(cfg, json.dumps(ent), flush=True)
     with open(out, "w") as f:

@@ -135,3 +135,12 @@ def test_no_cpu_fallback_in_product_path():
     with pytest.raises(ValueError):
         S.CsrSpmm(torch.zeros(2, dtype=torch.int32), torch.zeros(0, dtype=torch.int32),
                   torch.zeros(0), 1)
+
+
+def test_source_identity_of_the_build():
+    # the build's identity for evidence files (profiles/ncu_traffic.json): a hash of the sources, headers
+    # and flags -- stable across calls, sensitive to extra defines (nvcc .so files are not bit-reproducible)
+    a = spmm_build.source_sha16()
+    assert a == spmm_build.source_sha16() and len(a) == 16
+    assert spmm_build.source_sha16(defines=("MW_U=4",)) != a
+    assert os.path.join(spmm_build.ROOT, "include", "spmm.h") in spmm_build.DEPS
