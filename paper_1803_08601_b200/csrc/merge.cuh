@@ -20,6 +20,9 @@
 
 namespace spmm {
 
+constexpr int PART_ROWS = 16;  // k_partition: rows per thread and iteration
+constexpr int PART_MINB = 4;   // k_partition: resident CTAs per SM (register budget of PART_ROWS + 1 offsets)
+
 // states[2c] = row, states[2c+1] = nonzero, c in [0, num_ctas]: one pass over the rows instead of a
 // search per boundary.  2-D merge path: the row-end item of row r sits at path position
 // p_r = r + ro[r+1] (rows first on ties), so the boundary on diagonal d = c*I (< m + nnz) has consumed
@@ -28,8 +31,9 @@ namespace spmm {
 // the non-empty row r with ro[r] <= t < ro[r+1] (the largest r with ro[r] <= t).  Boundary 0 is
 // (0, 0) and boundary num_ctas is (m, nnz) in both.  Thread r reads ro[r], ro[r+1] (coalesced) and
 // writes the boundaries inside its row -- usually none or one; a row longer than I owns several.
+// (PART_ROWS rows per thread and iteration, their offsets loaded back to back.)
 // It also zeroes the compute kernel's task queue.
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS, PART_MINB)
 k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states,
             int* __restrict__ task_ctr) {
     const long long tid0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -42,15 +46,16 @@ k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int
     }
     const long long I = items;
     const long long last = (long long)num_ctas - 1;  // interior boundaries 1 .. num_ctas - 1
-    const long long stride = 4LL * gridDim.x * blockDim.x;
-    // 4 consecutive rows per thread and iteration: the 5 row offsets they need are loaded back to back
-    // (one memory round trip per iteration; lanes cover 4 x 32 consecutive rows)
-    for (long long r0 = 4 * tid0; r0 < m; r0 += stride) {
-        int o[5];
+    const long long stride = (long long)PART_ROWS * gridDim.x * blockDim.x;
+    // PART_ROWS consecutive rows per thread and iteration: the PART_ROWS + 1 row offsets they need are
+    // loaded back to back (one memory round trip per iteration, enough bytes in flight to stream the
+    // offsets of R-MAT 26 -- 268 MB -- near HBM speed with the grid capped at 8 CTAs per SM)
+    for (long long r0 = PART_ROWS * tid0; r0 < m; r0 += stride) {
+        int o[PART_ROWS + 1];
 #pragma unroll
-        for (int u = 0; u < 5; ++u) o[u] = (r0 + u <= m) ? __ldg(ro + r0 + u) : 0;
+        for (int u = 0; u <= PART_ROWS; ++u) o[u] = (r0 + u <= m) ? __ldg(ro + r0 + u) : 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < PART_ROWS; ++u) {
             const long long r = r0 + u;
             if (r >= m) break;
             const long long a = o[u], b = o[u + 1];
@@ -75,10 +80,10 @@ k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int
     }
 }
 
-// grid of k_partition: 4 rows per thread and iteration, at most 8 CTAs per SM
+// grid of k_partition: PART_ROWS rows per thread and iteration, one wave (PART_MINB CTAs per SM)
 inline unsigned partition_grid(long long m) {
-    const long long g = (m + 4LL * THREADS - 1) / (4LL * THREADS);
-    return (unsigned)(g < 1 ? 1 : (g > 8LL * 148 ? 8LL * 148 : g));
+    const long long g = (m + (long long)PART_ROWS * THREADS - 1) / ((long long)PART_ROWS * THREADS);
+    return (unsigned)(g < 1 ? 1 : (g > (long long)PART_MINB * 148 ? (long long)PART_MINB * 148 : g));
 }
 
 // FixCarryOut (Alg. 1 line 24): the first task of each run of equal carry rows sums the run in
