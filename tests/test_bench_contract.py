@@ -88,3 +88,25 @@ def test_torchrun_single_rank_exercises_the_distributed_path(cfg):
     assert d["n_gpus"] == 1 and d["value"] > 0
     assert d["config"]["bcast_B_ms"] is not None and d["config"]["allgather_C_ms"] is not None
     assert "NCCL broadcast" in d["e2e"]["includes"]
+
+
+def test_traffic_capture_matches_the_build_by_sources(tmp_path, monkeypatch):
+    # roofline.traffic comes from profiles/ncu_traffic.json; it counts as the same build when the library
+    # hash OR the source hash matches (nvcc .so files are not bit-reproducible), and never for a variant
+    # library selected with SPMM_LIB unless its own hash matches
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1803_08601_b200 import build as B
+    (tmp_path / "profiles").mkdir()
+    ent = {"dram_bytes": 1, "lib_sha16": "0" * 16, "src_sha16": B.source_sha16()}
+    (tmp_path / "profiles" / "ncu_traffic.json").write_text(json.dumps({"k": ent}))
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.delenv("SPMM_LIB", raising=False)
+    assert bench.load_traffic("k", "f" * 16)["same_build"] is True       # sources match
+    assert bench.load_traffic("k", "0" * 16)["same_build"] is True       # library matches
+    monkeypatch.setenv("SPMM_LIB", "/nonexistent/variant.so")
+    assert bench.load_traffic("k", "f" * 16)["same_build"] is False      # a variant: hash only
+    monkeypatch.delenv("SPMM_LIB")
+    ent["src_sha16"] = "1" * 16
+    (tmp_path / "profiles" / "ncu_traffic.json").write_text(json.dumps({"k": ent}))
+    assert bench.load_traffic("k", "f" * 16)["same_build"] is False      # stale capture
