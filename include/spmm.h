@@ -83,8 +83,7 @@ typedef struct {
                                 nnz >= 2^20), or
                                 the rows are too long to stage a 16-row tile (1.2 x 16 d > 8192),
                                 or (round-2 refit) mildly skewed rows (max row > 16 d, >= 256) with
-                                n >= 16, or very short rows with wide B (d < 3 and n >= 32, or
-                                d <= 4 and n > 64);
+                                n >= 16, or very short rows with wide B (d < 3 and n >= 32);
                                 costs one O(m) device reduction + stream sync at plan time.  */
     int32_t partition;       /* spmm_partition for the merge kernel: 2-D merge path over (row ends,
                                 nonzeros) (default) or the paper's 1-D nonzero split

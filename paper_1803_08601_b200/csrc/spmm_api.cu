@@ -66,6 +66,9 @@ namespace {
 #ifndef RS_DYN_SKEW
 #define RS_DYN_SKEW 4.0  // row split takes tiles from a queue when (AUTO) max row > RS_DYN_SKEW x mean row
 #endif
+#ifndef RS_G8_MAX_D
+#define RS_G8_MAX_D 64.0  // row split, n > 96: 8-lane groups up to this mean row length, 16 lanes above
+#endif
 #ifndef RS_GDIV
 #define RS_GDIV 2  // row split, 16..32 vector lanes per row: split the row over lanes/RS_GDIV lanes
 #endif
@@ -194,7 +197,7 @@ int pow2ceil(int x) {
     return p;
 }
 
-VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, bool folded) {
+VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, bool folded, double d = 0.0) {
     const uintptr_t pb = (uintptr_t)B, pc = (uintptr_t)C;
     int vec = 1;
     if (n % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && pb % 16 == 0 && pc % 16 == 0) vec = 4;
@@ -207,9 +210,10 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
         // column blocks each (n = 64: 8 lanes x 2 float4) -- more rows per warp, fewer broadcast loads
         const int G0 = std::min(32, pow2ceil(lanes));
         if (lanes <= 32 && G0 >= 16) {
-            // n = 97..128 with float4: 8 lanes x 4 blocks (4 rows per warp; measured 3% faster than 16 x 2
-            // on banded n = 128, profiles/r02_s3_experiments.txt); n = 64: 8 lanes x 2 blocks (4 x 4 slower)
-            c.G = (G0 == 32 && vec == 4 && lanes > 24) ? 8 : G0 / RS_GDIV;
+            // n = 97..128 with float4 and rows of <= 64 entries (d = mean row length): 8 lanes x 4 blocks
+            // (4 rows per warp; banded n = 128 3% faster than 16 x 2, short rows up to 1.7x; rows of
+            // 256+ entries 1.7-1.8x slower, profiles/r02_s3_experiments.txt); n = 64: 8 lanes x 2 blocks
+            c.G = (G0 == 32 && vec == 4 && lanes > 24 && d <= RS_G8_MAX_D) ? 8 : G0 / RS_GDIV;
             c.NV = (lanes + c.G - 1) / c.G;
         } else {
             c.G = G0;
@@ -224,6 +228,8 @@ VecCfg pick_vec(int n, const void* B, int64_t ldb, const void* C, int64_t ldc, b
     }
     return c;
 }
+
+inline double mean_row(const spmm_csr_s* h) { return h->m > 0 ? (double)h->nnz / (double)h->m : 0.0; }
 
 template <typename T, int SR>
 cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaStream_t st) {
@@ -374,7 +380,7 @@ cudaError_t run(const spmm_csr_s* h, const void* Bv, long long ldb, void* Cv, lo
     }
     if (h->chosen == SPMM_ALGO_ROWSPLIT) {
         P.tile_ctr = static_cast<int*>(ws);
-        return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true), P, st);
+        return launch_rowsplit<T, SR>(h, pick_vec(h->n, Bv, ldb, Cv, ldc, true, mean_row(h)), P, st);
     }
     const VecCfg mc = h->mfold ? pick_fold(h->n, Bv, ldb, Cv, ldc) : pick_vec(h->n, Bv, ldb, Cv, ldc, false);
     return launch_merge<T, SR>(h, mc, P, static_cast<unsigned char*>(ws), st);
@@ -559,7 +565,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             }
             const long long hmax = h->max_row;
             const bool skewed = (double)hmax > 16.0 * d && hmax >= 1024;
-            const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true);
+            const VecCfg rc = pick_vec(n, nullptr, n % 4 == 0 ? 4 : 1, nullptr, n % 4 == 0 ? 4 : 1, true, d);
             const long long groups = (long long)num_sms() * 2 * TE_CWARPS * (32 / rc.G);  // resident row groups
             // (only when there is enough work for idle row groups to matter: a small matrix is
             // launch-bound, and the single row-split launch beats merge's three -- config 0: 15 vs 51 us)
@@ -571,9 +577,10 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             // (round 2 refit on the config-3 sweep, profiles/r02_config3_summary.txt, with the task queue
             // and the lane-folded workers): merge path also wins for mildly skewed rows (max row above 16 d
             // but under the 1024 floor) once B rows are >= 64 bytes, and for very short rows with wide B
-            // (the row-split tiles then carry 1-4 nonzeros per row of per-row overhead)
+            // (the row-split tiles then carry 1-2 nonzeros per row of per-row overhead; d = 3-4 at n > 96
+            // went back to row split with its 8-lane x 4-block groups, profiles/r02_config3_summary.txt)
             const bool mild_skew = (double)hmax > 16.0 * d && hmax >= 256 && n >= 16;
-            const bool short_rows = (d < 3.0 && n >= 32) || (d <= 4.0 && n > 64);
+            const bool short_rows = d < 3.0 && n >= 32;
             pick = (skewed || few_rows || long_rows || mild_skew || short_rows) ? SPMM_ALGO_MERGE : SPMM_ALGO_ROWSPLIT;
             // dense-ish rows (NEXT-4): B streamed once per row tile beats a B-row gather
             // per nonzero once d is large (measured crossover)

@@ -1,7 +1,8 @@
 #!/bin/bash
 # final evidence of round 2 (session 3), part C, with the final build (k_partition 16 rows per thread):
 # full GPU suite, smoke, ncu traffic of the bench's kernels (profiles/ncu_traffic.json, with the source
-# hash), launch lists, bench lines, memcheck of the merge path, small-n AUTO table
+# hash), launch lists, bench lines, small-n AUTO table, BASELINE configs[3] sweep, scaling emulation
+# (compute-sanitizer is closed on this pool)
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 O=gpurun_out/final3c
 mkdir -p $O
@@ -24,5 +25,7 @@ timeout 900 python bench.py --config 2 --no-extras > $O/bench_c2.json 2> $O/benc
 timeout 900 python bench.py --config 1 --n 128 --no-extras --no-e2e > $O/bench_c1_n128.json 2> $O/bench_c1_n128.err; echo "bench c1 n128 rc=$?"
 cut -c1-400 $O/bench_default.json
 timeout 900 python scripts/exp_small_n.py 1,4,16,64 > $O/small_n.txt 2>&1; cat $O/small_n.txt
-timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --error-exitcode 99 --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "merge_partitions or partition_kernel or (merge_worker_parity and rmat12 and (f32_plus_times or i32_min_plus) and (1- or 16-)) or merge_task_queue or (adversarial and merge and (giant or rmat12 or many_empty or leading))" > $O/sanitize_memcheck_merge.log 2>&1; echo "memcheck rc=$?" >> $O/sanitize_memcheck_merge.log
-tail -3 $O/sanitize_memcheck_merge.log
+timeout 3000 python scripts/sweep_config4.py --out $O/config3 > $O/config3.log 2>&1; echo "config3 rc=$?"
+tail -8 $O/config3.log
+timeout 2400 python scripts/scaling_emulation.py --config 4 --out $O/scaling_emulation_config4 > $O/scaling4.log 2>&1; echo "scaling rc=$?"
+tail -7 $O/scaling4.log

@@ -309,7 +309,9 @@ def test_auto_refit_guards():
              (synth.lognormal_rows(1 << 16, 1 << 16, 7.92, 87), 4, "rowsplit"),
              (synth.uniform_rows(1 << 16, 1 << 16, 1, 5), 64, "merge"),
              (synth.uniform_rows(1 << 16, 1 << 16, 1, 5), 16, "rowsplit"),
-             (synth.uniform_rows(1 << 16, 1 << 16, 4, 5), 128, "merge"),
+             (synth.uniform_rows(1 << 16, 1 << 16, 2, 5), 128, "merge"),
+             # d = 4 at n = 128 went back to row split with the 8-lane x 4-block row groups (session 3)
+             (synth.uniform_rows(1 << 16, 1 << 16, 4, 5), 128, "rowsplit"),
              (synth.banded(1 << 16, 2, 2), 64, "rowsplit"))
     for pat, n, want in cases:
         vd = synth.values(pat.nnz, 1, "f32_plus_times").to(DEV)
