@@ -25,6 +25,10 @@
 #ifndef MW_MINB
 #define MW_MINB 5  // merge: 256-thread CTAs per SM (40 warps, <= 48 registers; 6 x 40 registers spills)
 #endif
+#ifndef MW_MINB1
+#define MW_MINB1 6  // merge, one value per lane (n <= 32): 48 warps (40 registers; spills only outside the
+                    // gather loop; R-MAT 22 n = 32 1.18 -> 1.09 ms, profiles/r02_s3_experiments.txt)
+#endif
 #ifndef MW_TPW
 #define MW_TPW 1  // merge: tasks per resident warp (1: one static task per warp; > 1: tasks from a queue)
 #endif

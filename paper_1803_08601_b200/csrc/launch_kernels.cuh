@@ -108,7 +108,7 @@ cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, in
     const bool epi = M && (M->epi.accumulate || M->epi.npeers);  // epilogue instances only when requested
     switch (cfg.vec * 10 + cfg.NV) {
         MW_CASE(4, 1, MW_U4, MW_MINB4) MW_CASE(2, 1, MW_U, MW_MINB) MW_CASE(2, 2, MW_U4, MW_MINB4)
-        MW_CASE(1, 1, MW_U, MW_MINB) MW_CASE(1, 2, MW_U, MW_MINB4) MW_CASE(1, 3, MW_U4, MW_MINB4)
+        MW_CASE(1, 1, MW_U, MW_MINB1) MW_CASE(1, 2, MW_U, MW_MINB4) MW_CASE(1, 3, MW_U4, MW_MINB4)
         MW_CASE(1, 4, MW_U4, MW_MINB4)
         default: return cudaErrorNotSupported;
     }

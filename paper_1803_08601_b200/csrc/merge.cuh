@@ -49,32 +49,27 @@ k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int
     const long long stride = (long long)PART_ROWS * gridDim.x * blockDim.x;
     // PART_ROWS consecutive rows per thread and iteration: the PART_ROWS + 1 row offsets they need are
     // loaded back to back (one memory round trip per iteration, enough bytes in flight to stream the
-    // offsets of R-MAT 26 -- 268 MB -- near HBM speed with the grid capped at 8 CTAs per SM)
+    // offsets of R-MAT 26 -- 268 MB -- with one wave of PART_MINB CTAs per SM)
     for (long long r0 = PART_ROWS * tid0; r0 < m; r0 += stride) {
         int o[PART_ROWS + 1];
 #pragma unroll
         for (int u = 0; u <= PART_ROWS; ++u) o[u] = (r0 + u <= m) ? __ldg(ro + r0 + u) : 0;
+        // the first boundary at or after this thread's first row: one division per PART_ROWS rows, then
+        // the rows are walked with D = c * I advancing by I (no per-row division)
+        long long c = (mode == 0) ? (r0 - 1 + o[0]) / I + 1  // first c with c*I > p_{r0-1} (p_{-1} = -1)
+                                  : (o[0] + I - 1) / I;      // first c with c*I >= ro[r0]
+        if (c < 1) c = 1;
+        long long D = c * I;
 #pragma unroll
         for (int u = 0; u < PART_ROWS; ++u) {
             const long long r = r0 + u;
             if (r >= m) break;
-            const long long a = o[u], b = o[u + 1];
-            long long c_lo, c_hi, base;
-            if (mode == 0) {
-                c_lo = (r - 1 + a) / I + 1;  // first c with c*I > p_{r-1} (p_{-1} = -1)
-                c_hi = (r + b) / I;          // last c with c*I <= p_r
-                base = -r;                   // nonzero = c*I - r
-            } else {
-                if (a >= b) continue;        // empty rows hold no nonzero boundary
-                c_lo = (a + I - 1) / I;
-                c_hi = (b - 1) / I;
-                base = 0;                    // nonzero = c*I
-            }
-            if (c_lo < 1) c_lo = 1;
-            if (c_hi > last) c_hi = last;
-            for (long long c = c_lo; c <= c_hi; ++c) {
+            // 2-D: boundaries with p_{r-1} < D <= p_r = r + ro[r+1] hold row r, nonzero D - r;
+            // 1-D: boundaries with ro[r] <= D < ro[r+1] hold row r, nonzero D (empty rows hold none)
+            const long long lim = (mode == 0) ? r + o[u + 1] + 1 : (long long)o[u + 1];
+            for (; c <= last && D < lim; ++c, D += I) {
                 states[2 * c] = (int)r;
-                states[2 * c + 1] = (int)(c * I + base);
+                states[2 * c + 1] = (int)((mode == 0) ? D - r : D);
             }
         }
     }
