@@ -31,7 +31,7 @@ constexpr int PART_MINB = 4;   // k_partition: resident CTAs per SM (register bu
 // the non-empty row r with ro[r] <= t < ro[r+1] (the largest r with ro[r] <= t).  Boundary 0 is
 // (0, 0) and boundary num_ctas is (m, nnz) in both.  Thread r reads ro[r], ro[r+1] (coalesced) and
 // writes the boundaries inside its row -- usually none or one; a row longer than I owns several.
-// (PART_ROWS rows per thread and iteration, their offsets loaded back to back.)
+// (PART_ROWS consecutive rows per thread and iteration.)
 // It also zeroes the compute kernel's task queue.
 __global__ void __launch_bounds__(THREADS, PART_MINB)
 k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int num_ctas, int* __restrict__ states,
@@ -46,14 +46,38 @@ k_partition(const int* __restrict__ ro, int m, int nnz, int items, int mode, int
     }
     const long long I = items;
     const long long last = (long long)num_ctas - 1;  // interior boundaries 1 .. num_ctas - 1
-    const long long stride = (long long)PART_ROWS * gridDim.x * blockDim.x;
-    // PART_ROWS consecutive rows per thread and iteration: the PART_ROWS + 1 row offsets they need are
-    // loaded back to back (one memory round trip per iteration, enough bytes in flight to stream the
-    // offsets of R-MAT 26 -- 268 MB -- with one wave of PART_MINB CTAs per SM)
-    for (long long r0 = PART_ROWS * tid0; r0 < m; r0 += stride) {
+    // a warp takes 32 x PART_ROWS consecutive rows per iteration; their offsets are loaded coalesced
+    // (one 128-byte line per load instruction) into a per-warp shared buffer, skewed by one word per 32
+    // so that lane l then reads its own PART_ROWS + 1 consecutive offsets (rows 16 l ..) without bank
+    // conflicts; the warp's loads are issued back to back (one memory round trip per iteration)
+    constexpr int WR = 32 * PART_ROWS;  // rows per warp and iteration
+    __shared__ int sro[WARPS_PER_CTA][WR + 1 + (WR + 1) / 32 + 1];
+    const int lane = threadIdx.x & 31;
+    int* so = sro[threadIdx.x >> 5];
+    const long long gwarp = tid0 >> 5;
+    const long long wstride = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long wb = gwarp * WR; wb < m; wb += wstride * WR) {
+        int v[PART_ROWS + 1];
+#pragma unroll
+        for (int k = 0; k <= PART_ROWS; ++k) {
+            const long long idx = wb + 32LL * k + lane;
+            v[k] = (idx <= m && (k < PART_ROWS || lane == 0)) ? __ldg(ro + idx) : 0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k <= PART_ROWS; ++k) {
+            const int i = 32 * k + lane;  // position i + i / 32
+            if (k < PART_ROWS || lane == 0) so[i + k] = v[k];
+        }
+        __syncwarp();
+        const long long r0 = wb + (long long)PART_ROWS * lane;
         int o[PART_ROWS + 1];
 #pragma unroll
-        for (int u = 0; u <= PART_ROWS; ++u) o[u] = (r0 + u <= m) ? __ldg(ro + r0 + u) : 0;
+        for (int u = 0; u <= PART_ROWS; ++u) {
+            const int i = PART_ROWS * lane + u;
+            o[u] = so[i + (i >> 5)];
+        }
+        if (r0 >= m) continue;
         // the first boundary at or after this thread's first row: one division per PART_ROWS rows, then
         // the rows are walked with D = c * I advancing by I (no per-row division)
         long long c = (mode == 0) ? (r0 - 1 + o[0]) / I + 1  // first c with c*I > p_{r0-1} (p_{-1} = -1)
