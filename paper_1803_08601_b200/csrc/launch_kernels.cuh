@@ -115,7 +115,7 @@ cudaError_t merge_w_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, in
 #undef MW_CASE
 }
 
-// dispatch over the k_merge_f instances (lane-folded merge, n <= MF_MAX_N): VEC in {1, 4}, G lanes per slot
+// dispatch over the k_merge_f instances (lane-folded merge, n <= MF_MAX_N): VEC in {1, 2, 4}, G lanes per slot
 template <typename T, int SR>
 cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, int* per_sm_out) {
 #define MF_CASE(V, G_, L_, MB_) \
@@ -127,6 +127,8 @@ cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, in
     // wider slots: L = 8 (profiles/r02_fold_tuning.txt)
     switch (cfg.vec * 100 + cfg.G) {
         MF_CASE(4, 1, MF_L_NARROW, MF_MINB4_NARROW) MF_CASE(4, 2, MF_L_NARROW, MF_MINB4_NARROW) MF_CASE(4, 4, MF_L, MF_MINB4)
+        MF_CASE(2, 1, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(2, 2, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(2, 4, MF_L, MF_MINB)
+        MF_CASE(2, 8, MF_L, MF_MINB)
         MF_CASE(1, 1, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(1, 2, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(1, 4, MF_L, MF_MINB)
         MF_CASE(1, 8, MF_L, MF_MINB) MF_CASE(1, 16, MF_L, MF_MINB)
         default: return cudaErrorNotSupported;

@@ -41,6 +41,10 @@ template <> __device__ __forceinline__ void mf_ldg<1>(unsigned (&o)[1], const vo
     asm volatile("{.reg .pred q; setp.ne.b32 q, %2, 0; mov.b32 %0, 0; @q ld.global.nc.b32 %0, [%1];}"
                  : "=r"(o[0]) : "l"(p), "r"((int)pred));
 }
+template <> __device__ __forceinline__ void mf_ldg<2>(unsigned (&o)[2], const void* p, bool pred) {
+    asm volatile("{.reg .pred q; setp.ne.b32 q, %3, 0; mov.b32 %0, 0; mov.b32 %1, 0; @q ld.global.nc.v2.b32 {%0, %1}, [%2];}"
+                 : "=r"(o[0]), "=r"(o[1]) : "l"(p), "r"((int)pred));
+}
 template <> __device__ __forceinline__ void mf_ldg<4>(unsigned (&o)[4], const void* p, bool pred) {
     asm volatile("{.reg .pred q; setp.ne.b32 q, %5, 0; mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;"
                  " @q ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];}"

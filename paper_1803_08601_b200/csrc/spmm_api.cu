@@ -263,7 +263,11 @@ cudaError_t launch_rowsplit(const spmm_csr_s* h, VecCfg cfg, TileParams P, cudaS
 VecCfg pick_fold(int n, const void* B, int64_t ldb, const void* C, int64_t ldc) {
     const uintptr_t pb = (uintptr_t)B, pc = (uintptr_t)C;
     VecCfg c;
-    c.vec = (n % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && pb % 16 == 0 && pc % 16 == 0) ? 4 : 1;
+    // float4 when n, ldb, ldc and the bases allow it, else float2 (n = 2: one lane per slot, 32 slots --
+    // half the chunk overhead of two scalar lanes), else scalar
+    if (n % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && pb % 16 == 0 && pc % 16 == 0) c.vec = 4;
+    else if (n % 2 == 0 && ldb % 2 == 0 && ldc % 2 == 0 && pb % 8 == 0 && pc % 8 == 0) c.vec = 2;
+    else c.vec = 1;
     c.G = pow2ceil((n + c.vec - 1) / c.vec);
     c.NV = 1;
     return c;
@@ -629,7 +633,7 @@ spmm_status spmm_csr_plan_ex(spmm_csr_t h, int32_t n, spmm_algo algo, spmm_semir
             // merge-path items per task (the partition granularity, Alg. 1 line 2): tpw tasks per
             // resident merge warp of the kernel instance this n uses with aligned B / C, so every warp
             // streams contiguous, equal slices of the path
-            const int l4 = n % 4 == 0 ? 4 : 1;
+            const int l4 = n % 4 == 0 ? 4 : (n % 2 == 0 ? 2 : 1);
             const VecCfg mc = fold ? pick_fold(n, nullptr, l4, nullptr, l4) : pick_vec(n, nullptr, l4, nullptr, l4, false);
             int per_sm = merge_per_sm_warps(h->dtype, sr, mc, fold);
             if (per_sm <= 0) per_sm = 32;

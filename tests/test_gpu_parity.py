@@ -601,7 +601,7 @@ _WP = {}
 @pytest.mark.parametrize("pat", ["rmat12", "lognormal", "many_empty_rows", "giant_row_plus_singletons",
                                  "leading_trailing_empty", "unsorted_duplicates"])
 @pytest.mark.parametrize("kind", synth.KINDS)
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 12, 13, 16])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 8, 10, 12, 13, 14, 16])
 @pytest.mark.parametrize("worker,tpw", [("folded", 1), ("folded", 4), ("warp", 4)])
 def test_merge_worker_parity(pat, kind, n, worker, tpw):
     if not _WP:
@@ -628,10 +628,10 @@ def test_folded_merge_partitions_and_task_sizes(partition, items, kind, n):
 @pytest.mark.parametrize("kind", synth.KINDS)
 def test_folded_merge_padding_and_misalignment(kind):
     """ldb/ldc padding (poisoned) and a misaligned B base: the folded kernel's scalar path (VEC = 1,
-    G up to 16 lanes per slot)."""
+    G up to 16 lanes per slot) and its float2 path on 8-byte aligned rows (VEC = 2)."""
     p = synth.rmat(11, 8, 41)
     for n, ldb, ldc, off in ((16, 16, 16, 1), (16, 20, 17, 0), (12, 12, 12, 3), (9, 11, 10, 0), (1, 3, 2, 1),
-                             (8, 8, 8, 2), (4, 4, 4, 1)):
+                             (8, 8, 8, 2), (4, 4, 4, 1), (2, 6, 4, 2), (10, 12, 10, 0), (6, 6, 8, 2)):
         val, Bh, ro, ci, vd, Bd, Cd = make_inputs(p, kind, n, ldb=ldb, ldc=ldc, b_offset=off)
         run_gpu(p, kind, n, "merge", ro, ci, vd, Bd, Cd, merge_worker="folded")
         check(p, kind, n, val, Bh, Cd)
