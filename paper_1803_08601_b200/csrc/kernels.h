@@ -62,6 +62,10 @@
 #ifndef MF_MINB_NARROW
 #define MF_MINB_NARROW 12  // merge, folded, 1-2 lanes per slot: CTAs per SM (48 warps)
 #endif
+#ifndef MF_L_NARROW4
+#define MF_L_NARROW4 6  // merge, folded, float4, 1-2 lanes per slot: items per slot per chunk (n = 8 R-MAT 22
+                        // 721 -> 637 us vs L = 4; with scalar / float2 slots L > 4 is slower)
+#endif
 #ifndef MF_MINB4_NARROW
 #define MF_MINB4_NARROW 8  // merge, folded, float4, 1-2 lanes per slot (4 values per gather: 64 registers)
 #endif

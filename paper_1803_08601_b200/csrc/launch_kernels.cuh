@@ -123,10 +123,11 @@ cudaError_t merge_f_launch(VecCfg cfg, const MergeParams* M, cudaStream_t st, in
         return epi ? launch_warp_tasks<k_merge_f<T, SR, V, G_, L_, MB_, true>, MF_THREADS>(M, st, per_sm_out)  \
                    : launch_warp_tasks<k_merge_f<T, SR, V, G_, L_, MB_, false>, MF_THREADS>(M, st, per_sm_out);
     const bool epi = M && (M->epi.accumulate || M->epi.npeers);
-    // 1-2 lanes per slot (n <= 2, or n <= 8 with float4): short chunks (L = 4) and more resident warps;
-    // wider slots: L = 8 (profiles/r02_fold_tuning.txt)
+    // 1-2 lanes per slot (n <= 2, or n <= 8 with float4): short chunks (L = 4; 6 with float4, which has
+    // the registers for it) and more resident warps; wider slots: L = 8 (profiles/r02_fold_tuning.txt,
+    // r02_s3_experiments.txt)
     switch (cfg.vec * 100 + cfg.G) {
-        MF_CASE(4, 1, MF_L_NARROW, MF_MINB4_NARROW) MF_CASE(4, 2, MF_L_NARROW, MF_MINB4_NARROW) MF_CASE(4, 4, MF_L, MF_MINB4)
+        MF_CASE(4, 1, MF_L_NARROW4, MF_MINB4_NARROW) MF_CASE(4, 2, MF_L_NARROW4, MF_MINB4_NARROW) MF_CASE(4, 4, MF_L, MF_MINB4)
         MF_CASE(2, 1, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(2, 2, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(2, 4, MF_L, MF_MINB)
         MF_CASE(2, 8, MF_L, MF_MINB)
         MF_CASE(1, 1, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(1, 2, MF_L_NARROW, MF_MINB_NARROW) MF_CASE(1, 4, MF_L, MF_MINB)
